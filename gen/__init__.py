@@ -101,6 +101,8 @@ def cuda_lib():
             L.gen_routing_cuda.argtypes = [u64, u64, i, i, i, i, i, i, i, vp, vp]
             L.gen_hidden_cuda.argtypes = [u64, u64, i, i, i, i, i, vp, vp]
             L.gen_wgate_cuda.argtypes = [u64, i, i, i, i, i, vp, vp]
+            L.gen_ids_to_mask_cuda.argtypes = [vp, ctypes.c_size_t, i, i, vp, vp]
+            L.gen_ids_to_mask_cuda.restype = ctypes.c_int
             for f in ("gen_trees_cuda", "gen_routing_cuda", "gen_hidden_cuda", "gen_wgate_cuda"):
                 getattr(L, f).restype = ctypes.c_int
             _cuda = L
@@ -239,5 +241,16 @@ def wgate_cuda(seed, L, E, d, mode=0, scale_log2=0, device="cuda"):
     import torch
     out = torch.empty((L, E, d), dtype=torch.bfloat16, device=device)
     rc = cuda_lib().gen_wgate_cuda(seed, L, E, d, mode, scale_log2, _tp(out), _stream())
+    assert rc == 0, rc
+    return out
+
+
+def ids_to_mask_cuda(ids, E):
+    """Device re-encoding of uint8 ids [B][N][L][K] into one-hot masks [B][N][L][EW] (int64)."""
+    import torch
+    B, N, L, K = ids.shape
+    EW = (E + 63) // 64
+    out = torch.empty((B, N, L, EW), dtype=torch.int64, device=ids.device)
+    rc = cuda_lib().gen_ids_to_mask_cuda(_tp(ids), B * N * L, K, EW, _tp(out), _stream())
     assert rc == 0, rc
     return out

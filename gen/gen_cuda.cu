@@ -73,9 +73,30 @@ __global__ void k_wgate(uint64_t seed, int L, int E, int d, int mode, int scale_
     }
 }
 
+__global__ void k_ids_to_mask(const uint8_t *ids, size_t rows, int K, int EW, uint64_t *mask)
+{
+    for (size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x; r < rows;
+         r += (size_t)gridDim.x * blockDim.x) {
+        uint64_t m[4] = {0, 0, 0, 0};
+        for (int j = 0; j < K; j++) {
+            int e = ids[r * K + j];
+            m[e >> 6] |= 1ull << (e & 63);
+        }
+        for (int w = 0; w < EW; w++) mask[r * EW + w] = m[w];
+    }
+}
+
 }  // namespace
 
 extern "C" {
+
+// one-hot routing masks [rows][EW] from uint8 ids [rows][K] (input re-encoding)
+int gen_ids_to_mask_cuda(const void *ids, size_t rows, int K, int EW, void *mask, cudaStream_t stream)
+{
+    k_ids_to_mask<<<148 * 16, 256, 0, stream>>>((const uint8_t *)ids, rows, K, EW, (uint64_t *)mask);
+    return (int)cudaGetLastError();
+}
+
 
 int gen_cuda_abi_version(void) { return 1; }
 

@@ -1,0 +1,252 @@
+/*
+ * evict.h — C ABI of the B200-native EVICT hot path (libevict.so).
+ *
+ * EVICT (arxiv 2605.00342, PAPER.md) truncates an EAGLE-style draft tree to
+ * its most cost-effective ancestor-closed prefix before MoE verification.
+ * Given a batch of draft trees (parent pointers + drafter probabilities q)
+ * and the offline-profiled cost table C(k), the calls below compute
+ *   evict_select            — Score(v) (Eq. 7), the ancestor-closed ranking
+ *                             (§3.2.1), Ê[A(T_k)] prefix sums (Eq. 8) and
+ *                             k* = argmax_k Ê[A(T_k)]/C(k) (Eq. 10, §3.2.3)
+ *   evict_build_verify_tree — the kept tree T_{k*} compacted into the verify
+ *                             batch: tree-attention mask, positions, retrieve
+ *                             indices, next-token/next-sibling lists (Fig. 4c)
+ *   evict_expert_union      — per-layer union of the MoE experts the kept
+ *                             nodes activate (Eq. 5), from routing ids/masks
+ *   evict_router_union      — the router logits W_g·h (Eq. 4) of the kept
+ *                             nodes on tcgen05 tensor cores, TopK, and the
+ *                             same union
+ *   evict_select_build_union— the three calls fused into one launch (same
+ *                             outputs as calling them in sequence)
+ *   evict_batch_stats       — aggregate statistics for the multi-GPU
+ *                             all-reduce.
+ *
+ * Conventions (every call):
+ *  - All array arguments are DEVICE pointers owned by the caller; the
+ *    library never allocates, frees or retains them.  Descriptor structs are
+ *    host memory, read during the call only.  `stream` is a cudaStream_t.
+ *  - Calls are stream-ordered and CUDA-graph capturable: no host sync, no
+ *    allocation, no device→host read (PAPER.md:198–204 graph fusion).
+ *  - Host-checkable argument errors return EVICT_ERR_INVALID_ARG (or
+ *    EVICT_ERR_UNSUPPORTED for a shape this build does not implement, or a
+ *    device that is not sm_100) and launch nothing.  Launch failures return
+ *    EVICT_ERR_CUDA.
+ *  - Data errors are reported per tree in `status` (bits EVICT_TREE_*), and
+ *    that tree's outputs are written in their defined error state (k* = 0,
+ *    empty keep set, zero rows); other trees are unaffected.
+ *  - Outputs are fully overwritten except the accumulating expert_hist.
+ *  - Layouts: a tree batch is [B][N] row-major with row stride N
+ *    (max_nodes); bit i of 64-bit word i/64 of a bitset refers to node
+ *    (or slot, or expert) i.  W = ceil(N/64), EW = ceil(E/64).
+ *  - Readings of points the paper leaves open (root score 1, tie rules,
+ *    cost domain, verify layout, …) are listed in DESIGN.md §3 (Z1–Z20).
+ */
+#ifndef EVICT_H
+#define EVICT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EVICT_ABI_VERSION 1
+#define EVICT_MAX_NODES 128   /* N ≤ 128 ⇒ W ≤ 2 mask words */
+#define EVICT_MAX_EXPERTS 256 /* Ling-flash-2.0 has 256 experts */
+#define EVICT_MAX_TOPK 16
+#define EVICT_MAX_LAYERS 128
+
+typedef enum {
+    EVICT_OK = 0,
+    EVICT_ERR_INVALID_ARG = 1,
+    EVICT_ERR_UNSUPPORTED = 2,
+    EVICT_ERR_CUDA = 3
+} evict_status_t;
+
+/* per-tree data-error bits, OR-ed into status[b] */
+#define EVICT_TREE_BAD_SIZE 0x01u   /* n_nodes[b] not in [1, N] */
+#define EVICT_TREE_BAD_PARENT 0x02u /* parent[0] != -1 or parent[i] not in [0, i) */
+#define EVICT_TREE_BAD_PROB 0x04u   /* q[i] NaN, < 0 or > 1 (i ≥ 1) */
+#define EVICT_TREE_BAD_COST 0x08u   /* cost[k-1] NaN or ≤ 0 for a k ≤ n, or cost[0] = +inf */
+#define EVICT_TREE_BAD_EXPERT 0x10u /* a kept node routes to an expert id outside [0, E) */
+#define EVICT_TREE_BAD_KEEP 0x20u   /* keep set misses the root, is not ancestor-closed, or keeps a pad */
+
+/* A batch of draft trees (the drafter's tree rooted at x_{t+1}).
+ * Nodes are numbered topologically: parent[0] = -1, 0 ≤ parent[i] < i.
+ * q[i] = q^T(v_i) = P_Md(v_i | x_{<v_i}); q[0] is ignored
+ * (the root is already committed, Score(root) = 1, reading Z1).           */
+typedef struct {
+    int32_t batch;           /* B ≥ 1 */
+    int32_t max_nodes;       /* N: row stride, 1..128, multiple of 4 */
+    const int32_t *n_nodes;  /* [B] real node count n_b ∈ [1, N], or NULL (= N) */
+    const int32_t *parent;   /* [B][N] int32 */
+    const float *q;          /* [B][N] fp32 */
+} evict_trees_t;
+
+/* ---------------------------------------------------------------------------
+ * evict_select — A1–A5 (§3.1–§3.2.3).
+ *   Score(v) = Π_{u∈Path(root,v)} q(u), fp32, one rounding per edge in
+ *     root→leaf order (Eq. 7; reading Z6).
+ *   order    = nodes by (Score desc, index asc): the top-k prune of §3.2.1;
+ *     every prefix is ancestor-closed (tie rule Z4).
+ *   S[k]     = Σ_{j<k} Score(order[j]) = Ê[A(T_k)] (Eq. 8), fp32.
+ *   k*       = smallest argmax_{1≤k≤n_b} S[k]/C(k) (Eq. 10; Z2, Z3).
+ * cost: fp32 C(k) at cost[k-1], k = 1..N, per tree at cost + b*cost_stride
+ *   (cost_stride 0 = one shared table).  C(k) ∈ (0, +inf]; +inf marks an
+ *   infeasible k (no verify graph of that length, Z10); cost[0] finite.
+ * Outputs: k_star [B] (0 on error), e_hat [B] = S[k*], utility [B] =
+ *   S[k*]/C(k*) (C_AR dropped, Z18), keep_bits [B][W] = order[0..k*).
+ *   Optional (NULL to skip): order [B][N] rank → node (-1 pad),
+ *   prefix_sums [B][N] S[k] at [k-1] (0 pad), status [B].
+ * ------------------------------------------------------------------------- */
+evict_status_t evict_select(const evict_trees_t *trees, const float *cost, int32_t cost_stride,
+                            int32_t *k_star, float *e_hat, float *utility, uint64_t *keep_bits,
+                            int32_t *order, float *prefix_sums, uint32_t *status, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * evict_build_verify_tree — A6 (Fig. 4(c); layout Z12).
+ * keep_bits [B][W]: any ancestor-closed node set containing the root.
+ * Packed verify layout: tree b owns rows [off_b, off_b + k_b) of every
+ * per-row output, k_b = |keep_b|, off = exclusive scan of k over the batch
+ * in tree order (single pass, decoupled look-back).  Capacity B*N rows.
+ * Within a tree, slots s = 0..k_b-1 follow ascending node index.
+ *   verify_offsets [B+1] off_b; verify_offsets[B] = total rows T
+ *   kept_index     [T] node index of slot s
+ *   retrieve_index [T] b*N + node: flat index of the row's node in [B][N]
+ *                      draft arrays (gather index for tokens/hidden states)
+ *   positions      [T] pos_offset[b] + depth(node) (pos_offset NULL ⇒ 0)
+ *   next_token     [T] smallest kept child slot, -1 if none
+ *   next_sibling   [T] smallest slot > s with the same parent, -1 if none
+ *   tree_mask      [T][W] bit j ⇔ slot j is an ancestor-or-self of slot s
+ *                      (tree part of the attention mask; prefix KV implicit)
+ * A tree with a bad status contributes 0 rows.  Any of the per-row outputs
+ * may be NULL.  workspace: device scratch of evict_workspace_bytes(B) bytes
+ * (cleared by the call itself with cudaMemsetAsync).
+ * ------------------------------------------------------------------------- */
+evict_status_t evict_build_verify_tree(const evict_trees_t *trees, const uint64_t *keep_bits,
+                                       const int32_t *pos_offset, int32_t *verify_offsets,
+                                       int32_t *kept_index, int32_t *retrieve_index,
+                                       int32_t *positions, int32_t *next_token,
+                                       int32_t *next_sibling, uint64_t *tree_mask,
+                                       uint32_t *status, void *workspace, size_t workspace_bytes,
+                                       void *stream);
+
+size_t evict_workspace_bytes(int32_t batch);
+
+/* ---------------------------------------------------------------------------
+ * evict_expert_union — A7 (Eq. 5; scope Z13, Z16).
+ * For each tree b and MoE layer l: union_count[b][l] = |∪_{v kept} E_l(v)|,
+ * root included; union_total[b] = Σ_l union_count[b][l].
+ * Routing input, node-major rows (only the kept nodes' rows are read):
+ *   EVICT_ID_U8 / EVICT_ID_I32: ids [B][N][L][K] — top-K expert ids
+ *   EVICT_ID_MASK:              masks [B][N][L][EW] uint64 — one-hot top-K
+ *                               sets (bit e ⇔ expert e routed)
+ * Outputs: union_count [B][L], union_total [B] (or NULL), union_bits
+ * [B][L][EW] (or NULL), expert_hist [L][E] int64 (or NULL; ACCUMULATES the
+ * number of trees whose layer-l union contains expert e), status [B] (or
+ * NULL; only EVICT_TREE_BAD_EXPERT / BAD_KEEP bits are produced here).
+ * ------------------------------------------------------------------------- */
+#define EVICT_ID_U8 1
+#define EVICT_ID_I32 4
+#define EVICT_ID_MASK 8
+
+typedef struct {
+    int32_t num_layers;  /* L ≥ 1, ≤ 128 */
+    int32_t num_experts; /* E ≥ 1, ≤ 256 */
+    int32_t top_k;       /* K, 1 ≤ K ≤ min(E, 16) (ignored for EVICT_ID_MASK) */
+    int32_t id_format;   /* EVICT_ID_U8 | EVICT_ID_I32 | EVICT_ID_MASK */
+    const void *ids;     /* see above */
+} evict_routing_t;
+
+evict_status_t evict_expert_union(const evict_trees_t *trees, const uint64_t *keep_bits,
+                                  const evict_routing_t *routing, int32_t *union_count,
+                                  int32_t *union_total, uint64_t *union_bits,
+                                  int64_t *expert_hist, uint32_t *status, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * evict_select_build_union — evict_select → evict_build_verify_tree →
+ * evict_expert_union in ONE launch (the per-tree state stays on chip).
+ * Semantics and outputs are exactly those of the three calls in sequence
+ * (status is the OR of the three); any optional output may be NULL.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    /* select */
+    int32_t *k_star;
+    float *e_hat;
+    float *utility;
+    uint64_t *keep_bits;
+    int32_t *order;
+    float *prefix_sums;
+    /* build */
+    const int32_t *pos_offset;
+    int32_t *verify_offsets;
+    int32_t *kept_index;
+    int32_t *retrieve_index;
+    int32_t *positions;
+    int32_t *next_token;
+    int32_t *next_sibling;
+    uint64_t *tree_mask;
+    /* union */
+    int32_t *union_count;
+    int32_t *union_total;
+    uint64_t *union_bits;
+    int64_t *expert_hist;
+    uint32_t *status;
+} evict_fused_out_t;
+
+evict_status_t evict_select_build_union(const evict_trees_t *trees, const float *cost,
+                                        int32_t cost_stride, const evict_routing_t *routing,
+                                        const evict_fused_out_t *out, void *workspace,
+                                        size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * evict_router_union — A8 → A7 (Eq. 4–5; Z14, Z15).
+ * For every packed verify row r < verify_offsets[B] (output of
+ * evict_build_verify_tree) and layer l: logits = W_g[l] · h[l][retrieve_index[r]]
+ * (bf16 × bf16 → fp32 on tcgen05 tensor cores), E(h) = TopK(logits, K) by
+ * (logit desc, expert asc); the ids are OR-ed into the union of the row's
+ * tree.  Outputs as evict_expert_union (union_bits is required here as the
+ * accumulator; it is cleared by the call).
+ *   hidden  bf16 [L][B*N][d]  per-layer hidden states of every draft node
+ *   w_gate  bf16 [L][E][d]    router weights, rows = expert centroids
+ *   topk_ids int32 [L][B*N][K] (or NULL): per packed row r, at [l][r][j]
+ * Supported: E = 128, d % 64 == 0, K ≤ 16.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    int32_t num_layers;
+    int32_t num_experts;
+    int32_t top_k;
+    int32_t hidden_dim;  /* d */
+    const void *hidden;  /* bf16 [L][B*N][d] */
+    const void *w_gate;  /* bf16 [L][E][d] */
+} evict_router_t;
+
+evict_status_t evict_router_union(const evict_trees_t *trees, const int32_t *verify_offsets,
+                                  const int32_t *retrieve_index, const evict_router_t *router,
+                                  int32_t *union_count, int32_t *union_total,
+                                  uint64_t *union_bits, int32_t *topk_ids, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * evict_batch_stats — A9 aggregate statistics (north_star: the only
+ * cross-GPU exchange is an all-reduce of these).  int64 stats[6 + N + L]:
+ *   [0] trees  [1] Σk*  [2] Σn  [3] Σunion_total  [4] trees with status ≠ 0
+ *   [5 .. 5+N]      k* histogram, bins 0..N (bin 0 = errored trees)
+ *   [6+N .. 6+N+L)  Σ union_count per layer
+ * double dstats[2]: Σ e_hat, Σ utility over trees with status 0.
+ * Overwrites stats/dstats.  union_count may be NULL (L = 0).
+ * ------------------------------------------------------------------------- */
+evict_status_t evict_batch_stats(int32_t batch, int32_t max_nodes, int32_t num_layers,
+                                 const int32_t *n_nodes, const int32_t *k_star,
+                                 const float *e_hat, const float *utility,
+                                 const int32_t *union_count, const uint32_t *status,
+                                 int64_t *stats, double *dstats, void *stream);
+
+const char *evict_status_string(evict_status_t s);
+int evict_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EVICT_H */

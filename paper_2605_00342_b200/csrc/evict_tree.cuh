@@ -1,0 +1,655 @@
+// evict_tree.cuh — warp-per-tree device building blocks of the EVICT hot path
+// (sm_100a).  One warp owns one draft tree; lane t owns the NPL consecutive
+// nodes i = t*NPL + r (blocked layout, so rows load as 8/16-byte vectors).
+// The tree is staged in registers + a small per-warp shared-memory slab;
+// nothing here touches the host.
+//
+//   A1 tree_load_validate  PAPER.md:48 (tree), readings Z4/Z9/Z10
+//   A2 tree_scores         Eq. 7: level-synchronous fp32
+//                          product root→leaf (exact serial order per node)
+//   A3 tree_rank           §3.2.1: warp bitonic sort of
+//                          64-bit keys (~bits(score) << 32 | index)
+//   A4/A5 tree_argmax      Eq. 8–10: shuffle scan,
+//                          IEEE division by C(k), argmax via __reduce_max_sync
+//   A6 tree_build          Fig. 4(c): __ballot/__popc slot
+//                          compaction, ancestor-or-self mask rows, child lists
+//   A7 tree_union          Eq. 5: OR of kept nodes' routing
+//                          into per-layer expert bitsets, __popcll counts
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "evict.h"
+
+namespace evict {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kWarps = 8;  // warps (= trees) per CTA tile
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <int NPL>
+struct Shape {
+    static constexpr int NMAX = 32 * NPL;          // nodes per warp
+    static constexpr int W = (NMAX + 63) / 64;     // 64-bit mask words
+    static constexpr int W32 = (NMAX + 31) / 32;   // 32-bit words
+};
+
+// Per-warp shared-memory slab.
+template <int NPL>
+struct WarpSlab {
+    static constexpr int NMAX = Shape<NPL>::NMAX;
+    static constexpr int W = Shape<NPL>::W;
+    float score[NMAX];          // A2 parent lookup
+    uint8_t rank[NMAX];         // A3 node → rank
+    uint8_t klist[NMAX];        // A7 slot → node
+    uint64_t row[NMAX][W];      // A6 mask rows by slot
+    uint64_t child[NMAX][W];    // A6 kept-children masks by slot
+};
+
+// Register state of one tree (per lane: its NPL nodes).
+template <int NPL>
+struct TreeState {
+    static constexpr int W = Shape<NPL>::W;
+    int par[NPL];
+    float q[NPL];
+    float sc[NPL];
+    int dep[NPL];
+    int n;
+    uint32_t status;
+    int kstar;
+    float ehat, util;
+    uint64_t keep[W];  // identical in every lane
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ uint64_t shfl_xor64(uint64_t v, int m)
+{
+    uint32_t lo = __shfl_xor_sync(kFull, (uint32_t)v, m);
+    uint32_t hi = __shfl_xor_sync(kFull, (uint32_t)(v >> 32), m);
+    return ((uint64_t)hi << 32) | lo;
+}
+
+template <int W>
+__device__ __forceinline__ bool bit_of(const uint64_t (&m)[W], int i)
+{
+    bool r = false;
+#pragma unroll
+    for (int w = 0; w < W; w++)
+        if ((i >> 6) == w) r = (m[w] >> (i & 63)) & 1ull;
+    return r;
+}
+
+// number of set bits of m strictly below position i (0 ≤ i ≤ 64W)
+template <int W>
+__device__ __forceinline__ int popc_below(const uint64_t (&m)[W], int i)
+{
+    int c = 0;
+#pragma unroll
+    for (int w = 0; w < W; w++) {
+        int lo = w * 64;
+        uint64_t mk = i >= lo + 64 ? ~0ull : (i <= lo ? 0ull : ((1ull << (i - lo)) - 1ull));
+        c += __popcll(m[w] & mk);
+    }
+    return c;
+}
+
+// ------------------------------------------------------------ A1: load + validate
+// Loads parent/q of tree b (row stride N) into the lane's registers and
+// checks the tree (BAD_SIZE / BAD_PARENT / BAD_PROB).  -0.0 → +0.0 (Z9).
+template <int NPL>
+__device__ __forceinline__ void tree_load_validate(TreeState<NPL> &t, const evict_trees_t &tr,
+                                                   const int32_t *__restrict__ parent,
+                                                   const float *__restrict__ q,
+                                                   const int32_t *__restrict__ n_nodes, int b,
+                                                   int N)
+{
+    const int lane = lane_id();
+    const int base = lane * NPL;
+    const size_t row = (size_t)b * N;
+    if (base < N) {
+        if constexpr (NPL == 4) {
+            int4 p4 = __ldg(reinterpret_cast<const int4 *>(parent + row + base));
+            float4 q4 = __ldg(reinterpret_cast<const float4 *>(q + row + base));
+            t.par[0] = p4.x; t.par[1] = p4.y; t.par[2] = p4.z; t.par[3] = p4.w;
+            t.q[0] = q4.x; t.q[1] = q4.y; t.q[2] = q4.z; t.q[3] = q4.w;
+        } else if constexpr (NPL == 2) {
+            int2 p2 = __ldg(reinterpret_cast<const int2 *>(parent + row + base));
+            float2 q2 = __ldg(reinterpret_cast<const float2 *>(q + row + base));
+            t.par[0] = p2.x; t.par[1] = p2.y;
+            t.q[0] = q2.x; t.q[1] = q2.y;
+        } else {
+            t.par[0] = __ldg(parent + row + base);
+            t.q[0] = __ldg(q + row + base);
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < NPL; r++) { t.par[r] = -1; t.q[r] = 0.f; }
+    }
+    t.n = n_nodes ? __ldg(n_nodes + b) : N;
+    uint32_t st = 0;
+    if (t.n < 1 || t.n > N) st = EVICT_TREE_BAD_SIZE;
+#pragma unroll
+    for (int r = 0; r < NPL; r++) {
+        const int i = base + r;
+        if (i < t.n) {
+            if (i == 0) {
+                if (t.par[r] != -1) st |= EVICT_TREE_BAD_PARENT;
+            } else {
+                if (t.par[r] < 0 || t.par[r] >= i) st |= EVICT_TREE_BAD_PARENT;
+                float qq = t.q[r];
+                if (!(qq >= 0.f && qq <= 1.f)) st |= EVICT_TREE_BAD_PROB;  // NaN fails both
+            }
+        }
+        if (t.q[r] == 0.f) t.q[r] = 0.f;  // canonicalise -0.0
+    }
+    t.status = __reduce_or_sync(kFull, st);
+    if (t.status & EVICT_TREE_BAD_SIZE) t.status = EVICT_TREE_BAD_SIZE;
+}
+
+// cost validation (BAD_COST) for k = 1..n.  cost[k-1] NaN or ≤ 0, or cost[0] = +inf.
+template <int NPL>
+__device__ __forceinline__ void tree_load_cost(float (&c)[NPL], TreeState<NPL> &t,
+                                               const float *__restrict__ cost)
+{
+    const int base = lane_id() * NPL;
+    uint32_t st = 0;
+#pragma unroll
+    for (int r = 0; r < NPL; r++) {
+        const int i = base + r;
+        c[r] = 1.f;
+        if (i < t.n) {
+            c[r] = __ldg(cost + i);
+            if (!(c[r] > 0.f)) st |= EVICT_TREE_BAD_COST;           // NaN or ≤ 0
+            if (i == 0 && c[r] == __int_as_float(0x7f800000)) st |= EVICT_TREE_BAD_COST;
+        }
+    }
+    t.status |= __reduce_or_sync(kFull, st);
+}
+
+// ------------------------------------------------------------ A2: path products
+// Level-synchronous: a node takes score[parent]·q once its parent is final,
+// so each Score(v) is the exact serial root→leaf fp32 product (Eq. 7).
+// dep = depth.  With SCORES = false only the depth is computed.
+template <int NPL, bool SCORES>
+__device__ __forceinline__ void tree_levels(TreeState<NPL> &t, WarpSlab<NPL> &sm)
+{
+    const int base = lane_id() * NPL;
+    bool done[NPL];
+#pragma unroll
+    for (int r = 0; r < NPL; r++) {
+        const int i = base + r;
+        done[r] = (i == 0) || (i >= t.n);
+        t.sc[r] = (i == 0) ? 1.f : 0.f;
+        t.dep[r] = 0;
+        sm.score[i] = (i == 0) ? 1.f : -1.f;
+    }
+    __syncwarp();
+    for (int it = 1;; it++) {
+        bool pending = false;
+        bool fresh[NPL];
+#pragma unroll
+        for (int r = 0; r < NPL; r++) {
+            fresh[r] = false;
+            if (!done[r]) {
+                float ps = sm.score[t.par[r]];
+                if (ps >= 0.f) {
+                    if constexpr (SCORES) {
+                        float s = __fmul_rn(ps, t.q[r]);
+                        t.sc[r] = (s == 0.f) ? 0.f : s;
+                    }
+                    t.dep[r] = it;
+                    fresh[r] = true;
+                } else {
+                    pending = true;
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < NPL; r++)
+            if (fresh[r]) {
+                sm.score[base + r] = SCORES ? t.sc[r] : 0.f;
+                done[r] = true;
+            }
+        __syncwarp();
+        if (!__any_sync(kFull, pending)) break;
+    }
+}
+
+// ------------------------------------------------------------ A3–A5
+// Ranks the nodes (bitonic sort), scans S[k], divides by C(k) and takes the
+// smallest argmax.  Fills t.kstar/ehat/util/keep; optionally writes order and
+// prefix sums (row of N entries).
+template <int NPL>
+__device__ __forceinline__ void tree_rank_argmax(TreeState<NPL> &t, WarpSlab<NPL> &sm,
+                                                 const float (&c)[NPL], int N,
+                                                 int32_t *__restrict__ order_row,
+                                                 float *__restrict__ prefix_row)
+{
+    constexpr int NMAX = Shape<NPL>::NMAX;
+    constexpr int W = Shape<NPL>::W;
+    constexpr int W32 = Shape<NPL>::W32;
+    const int lane = lane_id();
+    const int base = lane * NPL;
+
+    uint64_t key[NPL];
+#pragma unroll
+    for (int r = 0; r < NPL; r++) {
+        const int i = base + r;
+        key[r] = (i < t.n) ? (((uint64_t)(~__float_as_uint(t.sc[r])) << 32) | (uint32_t)i) : ~0ull;
+    }
+    // bitonic sort ascending on key == (score desc, index asc)
+#pragma unroll
+    for (int k = 2; k <= NMAX; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < NPL) {
+#pragma unroll
+                for (int r = 0; r < NPL; r++) {
+                    const int rp = r ^ j;
+                    if (rp > r) {
+                        const bool asc = (((base + r) & k) == 0);
+                        uint64_t a = key[r], bb = key[rp];
+                        const bool sw = asc ? (a > bb) : (a < bb);
+                        key[r] = sw ? bb : a;
+                        key[rp] = sw ? a : bb;
+                    }
+                }
+            } else {
+                const int lj = j / NPL;
+#pragma unroll
+                for (int r = 0; r < NPL; r++) {
+                    const int x = base + r;
+                    uint64_t o = shfl_xor64(key[r], lj);
+                    const bool take_min = (((x & j) == 0) == ((x & k) == 0));
+                    key[r] = take_min ? (o < key[r] ? o : key[r]) : (o > key[r] ? o : key[r]);
+                }
+            }
+        }
+    }
+    // position p = base + r now holds the p-th ranked node
+    float sp[NPL];
+    int node[NPL];
+#pragma unroll
+    for (int r = 0; r < NPL; r++) {
+        node[r] = (int)(uint32_t)key[r];   // pads: -1
+        sp[r] = __uint_as_float(~(uint32_t)(key[r] >> 32));
+        if (base + r < t.n) sm.rank[node[r]] = (uint8_t)(base + r);
+    }
+    // A4: S[k] = Σ_{j<k} Score(order[j])
+    float loc[NPL];
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < NPL; r++) {
+        acc = __fadd_rn(acc, sp[r]);
+        loc[r] = acc;
+    }
+    float incl = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        float v = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl = __fadd_rn(incl, v);
+    }
+    float excl = __shfl_up_sync(kFull, incl, 1);
+    if (lane == 0) excl = 0.f;
+    float S[NPL];
+    uint32_t Rb[NPL];
+    uint32_t best = 0;
+#pragma unroll
+    for (int r = 0; r < NPL; r++) {
+        S[r] = __fadd_rn(excl, loc[r]);
+        const bool v = base + r < t.n;
+        // A5: R[k] = S[k] / C(k), IEEE division (cost +inf ⇒ R = 0)
+        float R = v ? __fdiv_rn(S[r], c[r]) : 0.f;
+        Rb[r] = v ? __float_as_uint(R) : 0u;   // R ≥ 0 ⇒ bit order = value order
+        best = Rb[r] > best ? Rb[r] : best;
+    }
+    const uint32_t mx = __reduce_max_sync(kFull, best);
+    int rfirst = NPL;
+#pragma unroll
+    for (int r = NPL - 1; r >= 0; r--)
+        if (Rb[r] == mx && base + r < t.n) rfirst = r;
+    const unsigned has = __ballot_sync(kFull, rfirst < NPL);
+    const int wl = __ffs(has) - 1;               // smallest k wins ties (Z3)
+    const int rf = __shfl_sync(kFull, rfirst, wl);
+    float Sk = 0.f, Rk = 0.f;
+#pragma unroll
+    for (int r = 0; r < NPL; r++)
+        if (r == rf) { Sk = S[r]; Rk = __uint_as_float(Rb[r]); }
+    t.ehat = __shfl_sync(kFull, Sk, wl);
+    t.util = __shfl_sync(kFull, Rk, wl);
+    t.kstar = wl * NPL + rf + 1;
+
+    if (order_row != nullptr && base < N) {
+#pragma unroll
+        for (int r = 0; r < NPL; r++) {
+            order_row[base + r] = (base + r < t.n) ? node[r] : -1;
+            prefix_row[base + r] = (base + r < t.n) ? S[r] : 0.f;
+        }
+    }
+    __syncwarp();
+    // keep = order[0 .. k*): node i kept ⇔ rank(i) < k*
+    uint32_t local = 0;
+#pragma unroll
+    for (int r = 0; r < NPL; r++) {
+        const int i = base + r;
+        if (i < t.n && sm.rank[i] < t.kstar) local |= 1u << ((i & 31));
+    }
+    uint32_t wd[2 * W];
+#pragma unroll
+    for (int w = 0; w < 2 * W; w++) {
+        uint32_t mine = (w < W32 && (base >> 5) == w) ? local : 0u;
+        wd[w] = (w < W32) ? __reduce_or_sync(kFull, mine) : 0u;
+    }
+#pragma unroll
+    for (int w = 0; w < W; w++) t.keep[w] = (uint64_t)wd[2 * w] | ((uint64_t)wd[2 * w + 1] << 32);
+}
+
+// ------------------------------------------------------------ A6: verify tree
+// Requires t.par/t.dep/t.n and t.keep.  Checks the keep set (BAD_KEEP) and
+// returns k = |keep| (0 on error).  Row outputs are written by emit_build.
+template <int NPL>
+__device__ __forceinline__ int tree_check_keep(TreeState<NPL> &t)
+{
+    constexpr int W = Shape<NPL>::W;
+    const int base = lane_id() * NPL;
+    uint32_t bad = 0;
+#pragma unroll
+    for (int r = 0; r < NPL; r++) {
+        const int i = base + r;
+        const bool kp = bit_of<W>(t.keep, i);
+        if (i >= t.n && kp) bad = 1;
+        if (i == 0 && !kp) bad = 1;
+        if (i > 0 && i < t.n && kp && !bit_of<W>(t.keep, t.par[r])) bad = 1;
+    }
+    if (__any_sync(kFull, bad)) t.status |= EVICT_TREE_BAD_KEEP;
+    int k = 0;
+#pragma unroll
+    for (int w = 0; w < W; w++) k += __popcll(t.keep[w]);
+    return k;
+}
+
+template <int NPL>
+__device__ __forceinline__ void tree_build_emit(const TreeState<NPL> &t, WarpSlab<NPL> &sm, int k,
+                                                int b, int N, int off, int pos_off,
+                                                int32_t *__restrict__ kept_index,
+                                                int32_t *__restrict__ retrieve_index,
+                                                int32_t *__restrict__ positions,
+                                                int32_t *__restrict__ next_token,
+                                                int32_t *__restrict__ next_sibling,
+                                                uint64_t *__restrict__ tree_mask)
+{
+    constexpr int W = Shape<NPL>::W;
+    const int lane = lane_id();
+    const int base = lane * NPL;
+    bool kp[NPL];
+    int slot[NPL], pslot[NPL];
+    int maxd = 0;
+#pragma unroll
+    for (int r = 0; r < NPL; r++) {
+        const int i = base + r;
+        kp[r] = i < t.n && bit_of<W>(t.keep, i);
+        slot[r] = popc_below<W>(t.keep, i);
+        pslot[r] = (i > 0 && kp[r]) ? popc_below<W>(t.keep, t.par[r]) : -1;
+        if (kp[r]) {
+            maxd = t.dep[r] > maxd ? t.dep[r] : maxd;
+            sm.klist[slot[r]] = (uint8_t)i;
+        }
+    }
+    maxd = __reduce_max_sync(kFull, maxd);
+    // ancestor-or-self rows, one tree level at a time
+    for (int d = 0; d <= maxd; d++) {
+#pragma unroll
+        for (int r = 0; r < NPL; r++) {
+            if (kp[r] && t.dep[r] == d) {
+#pragma unroll
+                for (int w = 0; w < W; w++) {
+                    uint64_t v = (d == 0) ? 0ull : sm.row[pslot[r]][w];
+                    if ((slot[r] >> 6) == w) v |= 1ull << (slot[r] & 63);
+                    sm.row[slot[r]][w] = v;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    for (int s = lane; s < k; s += 32)
+#pragma unroll
+        for (int w = 0; w < W; w++) sm.child[s][w] = 0ull;
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < NPL; r++)
+        if (kp[r] && pslot[r] >= 0)
+            atomicOr(reinterpret_cast<unsigned long long *>(&sm.child[pslot[r]][slot[r] >> 6]),
+                     1ull << (slot[r] & 63));
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < NPL; r++) {
+        if (!kp[r]) continue;
+        const int s = slot[r];
+        const int rowi = off + s;
+        int nt = -1, ns = -1;
+#pragma unroll
+        for (int w = W - 1; w >= 0; w--) {
+            uint64_t cm = sm.child[s][w];
+            if (cm) nt = w * 64 + __ffsll((long long)cm) - 1;
+        }
+        if (pslot[r] >= 0) {
+#pragma unroll
+            for (int w = W - 1; w >= 0; w--) {
+                uint64_t cm = sm.child[pslot[r]][w];
+                const int lo = w * 64;
+                uint64_t above = (s + 1 <= lo) ? ~0ull : (s + 1 >= lo + 64 ? 0ull : (~0ull << (s + 1 - lo)));
+                cm &= above;
+                if (cm) ns = lo + __ffsll((long long)cm) - 1;
+            }
+        }
+        const int i = base + r;
+        if (kept_index) kept_index[rowi] = i;
+        if (retrieve_index) retrieve_index[rowi] = b * N + i;
+        if (positions) positions[rowi] = pos_off + t.dep[r];
+        if (next_token) next_token[rowi] = nt;
+        if (next_sibling) next_sibling[rowi] = ns;
+        if (tree_mask) {
+#pragma unroll
+            for (int w = 0; w < W; w++) tree_mask[(size_t)rowi * W + w] = sm.row[s][w];
+        }
+    }
+}
+
+// ------------------------------------------------------------ A7: expert union
+// Lane `lane` owns layers l = lane + 32c.  For every kept node (slot order,
+// sm.klist), the node's routing row is read and OR-ed into the lane's
+// per-layer EW-word expert bitsets; counts are __popcll of the bitsets.
+template <int EW>
+struct LayerBits {
+    uint64_t w[EW];
+};
+
+template <int EW>
+__device__ __forceinline__ void or_id(LayerBits<EW> &bs, uint32_t e, uint32_t &bad, uint32_t E)
+{
+    bad |= (e >= E);
+    const uint64_t x = 1ull << (e & 63);
+#pragma unroll
+    for (int w = 0; w < EW; w++)
+        if ((e >> 6) == (uint32_t)w) bs.w[w] |= x;
+}
+
+// IDF: 1 = u8 ids, 4 = i32 ids, 8 = masks.  KT: compile-time K (0 = runtime).
+template <int NPL, int IDF, int KT, int EW, int CL>
+__device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL> &sm, int k,
+                                           int b, int N, int L, int K, int E, int idb,
+                                           const void *__restrict__ ids,
+                                           int32_t *__restrict__ union_count,
+                                           int32_t *__restrict__ union_total,
+                                           uint64_t *__restrict__ union_bits,
+                                           int64_t *__restrict__ expert_hist)
+{
+    const int lane = lane_id();
+    LayerBits<EW> bs[CL];
+#pragma unroll
+    for (int c = 0; c < CL; c++)
+#pragma unroll
+        for (int w = 0; w < EW; w++) bs[c].w[w] = 0ull;
+    uint32_t bad = 0;
+    const int Kr = KT ? KT : K;
+    if (!status) {
+        constexpr int U = 4;  // rows in flight per lane
+        for (int j0 = 0; j0 < k; j0 += U) {
+            if constexpr (IDF == 1 && KT == 8) {
+                uint2 v[U][CL];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int j = j0 + u;
+                    const int node = j < k ? sm.klist[j] : 0;
+                    const uint8_t *rowp = (const uint8_t *)ids + ((size_t)b * N + node) * L * 8;
+#pragma unroll
+                    for (int c = 0; c < CL; c++) {
+                        const int l = lane + 32 * c;
+                        v[u][c] = (j < k && l < L) ? __ldg(reinterpret_cast<const uint2 *>(rowp + l * 8))
+                                                   : make_uint2(0, 0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int c = 0; c < CL; c++) {
+                        if (j0 + u >= k || lane + 32 * c >= L) continue;
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            const uint32_t wv = h ? v[u][c].y : v[u][c].x;
+#pragma unroll
+                            for (int s = 0; s < 4; s++) or_id<EW>(bs[c], (wv >> (8 * s)) & 0xffu, bad, E);
+                        }
+                    }
+            } else if constexpr (IDF == 4 && KT == 8) {
+                int4 v[U][CL][2];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int j = j0 + u;
+                    const int node = j < k ? sm.klist[j] : 0;
+                    const int32_t *rowp = (const int32_t *)ids + ((size_t)b * N + node) * L * 8;
+#pragma unroll
+                    for (int c = 0; c < CL; c++) {
+                        const int l = lane + 32 * c;
+                        const bool ok = j < k && l < L;
+#pragma unroll
+                        for (int h = 0; h < 2; h++)
+                            v[u][c][h] = ok ? __ldg(reinterpret_cast<const int4 *>(rowp + l * 8) + h)
+                                            : make_int4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int c = 0; c < CL; c++) {
+                        if (j0 + u >= k || lane + 32 * c >= L) continue;
+#pragma unroll
+                        for (int h = 0; h < 2; h++) {
+                            or_id<EW>(bs[c], (uint32_t)v[u][c][h].x, bad, E);
+                            or_id<EW>(bs[c], (uint32_t)v[u][c][h].y, bad, E);
+                            or_id<EW>(bs[c], (uint32_t)v[u][c][h].z, bad, E);
+                            or_id<EW>(bs[c], (uint32_t)v[u][c][h].w, bad, E);
+                        }
+                    }
+            } else if constexpr (IDF == 8) {
+                uint64_t v[U][CL][EW];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int j = j0 + u;
+                    const int node = j < k ? sm.klist[j] : 0;
+                    const uint64_t *rowp = (const uint64_t *)ids + ((size_t)b * N + node) * L * EW;
+#pragma unroll
+                    for (int c = 0; c < CL; c++) {
+                        const int l = lane + 32 * c;
+                        const bool ok = j < k && l < L;
+                        if constexpr (EW == 2) {
+                            ulonglong2 x = ok ? __ldg(reinterpret_cast<const ulonglong2 *>(rowp + l * 2))
+                                              : make_ulonglong2(0, 0);
+                            v[u][c][0] = x.x;
+                            v[u][c][1] = x.y;
+                        } else {
+#pragma unroll
+                            for (int w = 0; w < EW; w++) v[u][c][w] = ok ? __ldg(rowp + l * EW + w) : 0ull;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int c = 0; c < CL; c++)
+#pragma unroll
+                        for (int w = 0; w < EW; w++) bs[c].w[w] |= v[u][c][w];
+            } else {
+                // generic K (any ≤ 16), u8 or i32: scalar loads
+#pragma unroll 1
+                for (int u = 0; u < U; u++) {
+                    const int j = j0 + u;
+                    if (j >= k) break;
+                    const int node = sm.klist[j];
+#pragma unroll
+                    for (int c = 0; c < CL; c++) {
+                        const int l = lane + 32 * c;
+                        if (l >= L) continue;
+                        const size_t o = (((size_t)b * N + node) * L + l) * Kr;
+                        for (int x = 0; x < Kr; x++) {
+                            uint32_t e = idb == 1 ? (uint32_t)__ldg((const uint8_t *)ids + o + x)
+                                                  : (uint32_t)__ldg((const int32_t *)ids + o + x);
+                            or_id<EW>(bs[c], e, bad, E);
+                        }
+                    }
+                }
+            }
+        }
+        if constexpr (IDF == 8) {
+            // bits at or above E are not experts
+#pragma unroll
+            for (int c = 0; c < CL; c++)
+#pragma unroll
+                for (int w = 0; w < EW; w++) {
+                    const int lo = w * 64;
+                    uint64_t valid = E >= lo + 64 ? ~0ull : (E <= lo ? 0ull : ((1ull << (E - lo)) - 1ull));
+                    if (bs[c].w[w] & ~valid) bad = 1;
+                }
+        }
+        if (__any_sync(kFull, bad)) status |= EVICT_TREE_BAD_EXPERT;
+    }
+    int tot = 0;
+    const bool zero = status != 0;
+#pragma unroll
+    for (int c = 0; c < CL; c++) {
+        const int l = lane + 32 * c;
+        if (l >= L) continue;
+        int cnt = 0;
+#pragma unroll
+        for (int w = 0; w < EW; w++) {
+            if (zero) bs[c].w[w] = 0ull;
+            cnt += __popcll(bs[c].w[w]);
+        }
+        tot += cnt;
+        union_count[(size_t)b * L + l] = cnt;
+        const int EWr = (E + 63) / 64;
+        if (union_bits) {
+#pragma unroll
+            for (int w = 0; w < EW; w++)
+                if (w < EWr) union_bits[((size_t)b * L + l) * EWr + w] = bs[c].w[w];
+        }
+        if (expert_hist && !zero) {
+#pragma unroll
+            for (int w = 0; w < EW; w++) {
+                uint64_t m = bs[c].w[w];
+                while (m) {
+                    const int e = w * 64 + __ffsll((long long)m) - 1;
+                    m &= m - 1;
+                    atomicAdd(reinterpret_cast<unsigned long long *>(expert_hist + (size_t)l * E + e), 1ull);
+                }
+            }
+        }
+    }
+    tot = __reduce_add_sync(kFull, tot);
+    if (union_total && lane == 0) union_total[b] = tot;
+}
+
+}  // namespace evict

@@ -1,0 +1,314 @@
+"""CUDA path vs oracle, element by element, through the C ABI (needs a B200).
+
+Inputs are seeded (gen/) or hand-made adversarial trees; the oracle runs on the
+same host arrays.  Bar: bit-exact integers; fp32 values within 1e-5 relative;
+near-ties reported as ties (oracle/parity.py).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from oracle.parity import compare_build, compare_select, compare_union
+
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "toy_tree.json")))
+
+
+@pytest.fixture(scope="module")
+def ev():
+    import torch  # noqa: F401
+    import paper_2605_00342_b200 as ev
+    ev.lib()
+    return ev
+
+
+def T(a, dtype=None):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.cuda()
+
+
+def npy(d):
+    return {k: (v.cpu().numpy() if hasattr(v, "cpu") else v) for k, v in d.items()}
+
+
+def pad_batch(trees, N):
+    B = len(trees)
+    P = np.full((B, N), -1, np.int32)
+    Q = np.zeros((B, N), np.float32)
+    n = np.zeros(B, np.int32)
+    for b, (p, q) in enumerate(trees):
+        P[b, :len(p)] = p
+        Q[b, :len(q)] = q
+        n[b] = len(p)
+    return P, Q, n
+
+
+def adversarial(N, rng):
+    out = []
+    out.append((np.arange(-1, N - 1, dtype=np.int32), np.full(N, 0.9, np.float32)))        # chain
+    out.append((np.array([-1] + [0] * (N - 1), np.int32), rng.uniform(0, 1, N).astype(np.float32)))  # star
+    p = np.array([-1] + [int(rng.integers(0, i)) for i in range(1, N)], np.int32)
+    out.append((p, np.ones(N, np.float32)))                                                  # q = 1 ties
+    out.append((p, np.zeros(N, np.float32)))                                                 # q = 0
+    q = np.full(N, 0.5, np.float32)
+    q[1:] = rng.choice([0.5, 0.25, 1.0, 0.0, -0.0], N - 1)
+    out.append((p, q))                                                                       # dyadic ties, -0
+    out.append((np.arange(-1, N - 1, dtype=np.int32), np.full(N, 2.0 ** -10, np.float32)))  # subnormal chain
+    for m in (1, 2, 3, N // 2, N - 1):
+        pp = np.array([-1] + [int(rng.integers(0, i)) for i in range(1, m)], np.int32)
+        out.append((pp, rng.uniform(0, 1, m).astype(np.float32)))                            # ragged n
+    for _ in range(10):
+        out.append((p, np.concatenate([[1], rng.choice([0.5, 0.25, 0.75, 1.0], N - 1)]).astype(np.float32)))
+    for _ in range(10):
+        out.append((p, rng.uniform(0, 1, N).astype(np.float32)))
+    for q in out:
+        q[1][0] = 1.0
+    return out
+
+
+def run_select(ev, P, Q, n, cost, cost_stride=0):
+    g = ev.evict_select(T(P), T(Q), T(cost), n_nodes=T(n), cost_stride=cost_stride, with_order=True)
+    return npy(g)
+
+
+def check_select(o, g, n):
+    res, msgs = compare_select(o, g, n_nodes=n, check_order=True)
+    assert not msgs, msgs[:5]
+    return res
+
+
+# ------------------------------------------------------------------ select
+def test_toy_tree(ev):
+    P, Q, n = pad_batch([(np.array(GOLD["parent"], np.int32), np.array(GOLD["q"], np.float32))], 8)
+    for cost in [GOLD["cost"]] + [v["cost"] for v in GOLD["cost_variants"].values()]:
+        c = np.array(cost, np.float32)
+        g = run_select(ev, P, Q, n, c)
+        o = oracle.select(P, Q, c, n_nodes=n)
+        check_select(o, g, n)
+    g = run_select(ev, P, Q, n, np.array(GOLD["cost"], np.float32))
+    assert g["k_star"][0] == 3 and int(g["keep_bits"][0, 0]) == 11
+    assert g["order"][0].tolist() == GOLD["order"]
+    assert g["e_hat"][0] == 2.125
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c4_60", "paper"])
+def test_select_generated(ev, name):
+    c = gen.CONFIGS[name]
+    B = max(c["B"], 256)
+    P, Q, n = gen.trees(c["seed"], B, c["N"], c["steps"], c["topk"])
+    cost = gen.cost_table(c["N"])
+    g = run_select(ev, P, Q, n, cost)
+    o = oracle.select(P, Q, cost, n_nodes=n, threads=8)
+    res = check_select(o, g, n)
+    assert res["match"] + res["tie"] == B
+
+
+@pytest.mark.parametrize("N", [4, 8, 32, 60, 64, 100, 128])
+def test_select_adversarial(ev, N):
+    rng = np.random.default_rng(N)
+    trees = adversarial(N, rng)
+    P, Q, n = pad_batch(trees, N)
+    # per-tree cost tables: default, constant, linear, infeasible entries
+    B = len(trees)
+    C = np.tile(gen.cost_table(N), (B, 1))
+    C[1::4] = 3.0
+    C[2::4] = 0.37 * np.arange(1, N + 1)
+    C[3::4, 2::3] = np.inf
+    g = run_select(ev, P, Q, n, C.astype(np.float32), cost_stride=N)
+    o = oracle.select(P, Q, C, n_nodes=n, cost_stride=N)
+    check_select(o, g, n)
+
+
+def test_select_invalid_inputs(ev):
+    N = 8
+    base_p = np.array([-1, 0, 0, 1, 1, 2, 3, 4], np.int32)
+    base_q = np.array(GOLD["q"], np.float32)
+    cases = []
+    p = base_p.copy(); p[0] = 0; cases.append((p, base_q))
+    p = base_p.copy(); p[5] = 5; cases.append((p, base_q))
+    q = base_q.copy(); q[3] = 1.5; cases.append((base_p, q))
+    q = base_q.copy(); q[3] = np.nan; cases.append((base_p, q))
+    q = base_q.copy(); q[3] = -0.25; cases.append((base_p, q))
+    cases.append((base_p, base_q))
+    P, Q, n = pad_batch(cases, N)
+    n = np.concatenate([n, [0, 9]]).astype(np.int32)
+    P = np.concatenate([P, P[:2]])
+    Q = np.concatenate([Q, Q[:2]])
+    C = np.tile(np.array(GOLD["cost"], np.float32), (len(n), 1))
+    g = run_select(ev, P, Q, n, C, cost_stride=N)
+    o = oracle.select(P, Q, C, n_nodes=n, cost_stride=N)
+    check_select(o, g, n)
+    assert (g["status"][:5] != 0).all() and g["status"][5] == 0 and (g["status"][6:] == 1).all()
+    # bad cost tables
+    C2 = np.tile(np.array(GOLD["cost"], np.float32), (3, 1))
+    C2[0, 4] = 0.0
+    C2[1, 0] = np.inf
+    C2[2, 7] = np.nan
+    P3, Q3, n3 = pad_batch([(base_p, base_q)] * 3, N)
+    g = run_select(ev, P3, Q3, n3, C2, cost_stride=N)
+    assert (g["status"] == 8).all() and (g["k_star"] == 0).all()
+
+
+def test_select_host_errors(ev):
+    import torch
+    P = torch.zeros((2, 6), dtype=torch.int32, device="cuda")           # N % 4 != 0
+    Q = torch.zeros((2, 6), dtype=torch.float32, device="cuda")
+    with pytest.raises(ev.EvictError) as e:
+        ev.evict_select(P, Q, torch.ones(6, device="cuda"))
+    assert e.value.code == ev.EVICT_ERR_INVALID_ARG
+
+
+# ------------------------------------------------------------------ build
+@pytest.mark.parametrize("name", ["c2", "c4", "c4_60"])
+def test_build_generated(ev, name):
+    c = gen.CONFIGS[name]
+    B = max(c["B"], 300)
+    P, Q, n = gen.trees(c["seed"] + 1, B, c["N"], c["steps"], c["topk"])
+    o = oracle.select(P, Q, gen.cost_table(c["N"]), n_nodes=n)
+    keep = o["keep_bits"]
+    pos = np.arange(B, dtype=np.int32) * 3 + 100
+    ob = oracle.build_verify_tree(P, keep, n_nodes=n, pos_offset=pos)
+    gb = npy(ev.evict_build_verify_tree(T(P), T(keep.view(np.int64)), n_nodes=T(n), pos_offset=T(pos)))
+    assert not compare_build(ob, gb)
+
+
+@pytest.mark.parametrize("N", [8, 60, 128])
+def test_build_adversarial_keep_sets(ev, N):
+    rng = np.random.default_rng(N + 7)
+    trees = adversarial(N, rng)
+    P, Q, n = pad_batch(trees, N)
+    B = len(trees)
+    W = (N + 63) // 64
+    keep = np.zeros((B, W), np.uint64)
+    for b in range(B):
+        nb = int(n[b])
+        mode = b % 4
+        if mode == 0:
+            kept = range(nb)                                   # full tree
+        elif mode == 1:
+            kept = [0]
+        elif mode == 2:                                        # random ancestor-closed
+            s = {0}
+            for v in range(1, nb):
+                if P[b, v] in s and rng.uniform() < 0.6:
+                    s.add(v)
+            kept = sorted(s)
+        else:                                                  # invalid: child without parent
+            kept = [0] + ([nb - 1] if nb > 2 and P[b, nb - 1] != 0 else [])
+        for v in kept:
+            keep[b, v // 64] |= np.uint64(1 << (v % 64))
+    ob = oracle.build_verify_tree(P, keep, n_nodes=n)
+    gb = npy(ev.evict_build_verify_tree(T(P), T(keep.view(np.int64)), n_nodes=T(n)))
+    assert not compare_build(ob, gb)
+
+
+def test_build_large_batch_offsets(ev):
+    """Decoupled look-back across many tiles and persistent CTAs."""
+    B, N = 50_000, 60
+    P, Q, n = gen.trees(77, B, N, 6, 10)
+    o = oracle.select(P, Q, gen.cost_table(N), n_nodes=n, threads=8)
+    ob = oracle.build_verify_tree(P, o["keep_bits"], n_nodes=n)
+    gb = npy(ev.evict_build_verify_tree(T(P), T(o["keep_bits"].view(np.int64)), n_nodes=T(n)))
+    assert not compare_build(ob, gb)
+
+
+# ------------------------------------------------------------------ union
+@pytest.mark.parametrize("fmt", ["u8", "i32", "mask"])
+@pytest.mark.parametrize("shape", [(60, 48, 128, 8), (60, 94, 128, 8), (128, 48, 256, 8),
+                                   (8, 2, 8, 2), (60, 5, 64, 3), (32, 33, 200, 6)])
+def test_union(ev, fmt, shape):
+    N, L, E, K = shape
+    if fmt == "u8" and E > 256:
+        pytest.skip()
+    B = 80
+    steps, topk = (6, 10) if N >= 32 else (3, 2)
+    P, Q, n = gen.trees(5, B, N, steps, topk)
+    o = oracle.select(P, Q, gen.cost_table(N), n_nodes=n)
+    ids = gen.routing(9, B, N, L, E, K, dtype=np.uint8 if fmt == "u8" else np.int32)
+    ou = oracle.expert_union(o["keep_bits"], ids, E, n_nodes=n)
+    if fmt == "mask":
+        dev_ids = T(gen.ids_to_mask(ids, E).view(np.int64))
+    else:
+        dev_ids = T(ids)
+    gu = npy(ev.evict_expert_union(T(o["keep_bits"].view(np.int64)), dev_ids, E, n_nodes=T(n)))
+    assert not compare_union(ou, gu)
+
+
+def test_union_bad_expert_and_hist(ev):
+    import torch
+    B, N, L, E, K = 16, 8, 3, 16, 2
+    ids = np.zeros((B, N, L, K), np.int32)
+    rng = np.random.default_rng(0)
+    for b in range(B):
+        for v in range(N):
+            for l in range(L):
+                ids[b, v, l] = rng.permutation(E)[:K]
+    ids[3, 0, 1, 0] = 99                      # kept root: bad
+    ids[4, 7, 1, 0] = 99                      # pruned node: ignored
+    keep = np.full((B, 1), 0b0111_1111, np.uint64)
+    ou = oracle.expert_union(keep, ids, E)
+    hist = torch.zeros((L, E), dtype=torch.int64, device="cuda")
+    gu = npy(ev.evict_expert_union(T(keep.view(np.int64)), T(ids), E, expert_hist=hist))
+    assert not compare_union(ou, gu)
+    assert gu["status"][3] == 0x10 and gu["status"][4] == 0
+    h = np.zeros((L, E), np.int64)
+    for b in range(B):
+        if ou["status"][b]:
+            continue
+        for l in range(L):
+            for e in range(E):
+                if (int(ou["union_bits"][b, l, 0]) >> e) & 1:
+                    h[l, e] += 1
+    assert (hist.cpu().numpy() == h).all()
+
+
+# ------------------------------------------------------------------ fused
+@pytest.mark.parametrize("name,fmt", [("c2", "u8"), ("c4", "u8"), ("c4_60", "i32"),
+                                      ("c4_60", "mask"), ("paper", "u8")])
+def test_fused_equals_oracle(ev, name, fmt):
+    c = gen.CONFIGS[name]
+    B = 333
+    N, L, E, K = c["N"], c["L"], c["E"], c["K"]
+    P, Q, n = gen.trees(c["seed"] + 11, B, N, c["steps"], c["topk"])
+    n[::7] = np.maximum(1, n[::7] // 2)                     # ragged
+    cost = gen.cost_table(N)
+    ids = gen.routing(c["seed"], B, N, L, E, K, dtype=np.int32 if fmt == "i32" else np.uint8)
+    dev_ids = T(gen.ids_to_mask(ids, E).view(np.int64)) if fmt == "mask" else T(ids)
+    pos = np.full(B, 5, np.int32)
+    g = npy(ev.evict_select_build_union(T(P), T(Q), T(cost), dev_ids, E, n_nodes=T(n),
+                                        pos_offset=T(pos), with_bits=True, with_order=True))
+    o = oracle.select(P, Q, cost, n_nodes=n, threads=8)
+    res, msgs = compare_select(o, g, n_nodes=n, check_order=True)
+    assert not msgs, msgs[:5]
+    keep = g["keep_bits"].view(np.uint64)
+    ob = oracle.build_verify_tree(P, keep, n_nodes=n, pos_offset=pos)
+    assert not compare_build(ob, {k: v for k, v in g.items() if k != "status"})
+    ou = oracle.expert_union(keep, ids, E, n_nodes=n, threads=8)
+    assert not compare_union(ou, g)
+
+
+# ------------------------------------------------------------------ stats
+def test_batch_stats(ev):
+    B, N, L, E, K = 5000, 60, 48, 128, 8
+    P, Q, n = gen.trees(3, B, N, 6, 10)
+    Q[17, 5] = 2.0                                           # one bad tree
+    cost = gen.cost_table(N)
+    ids = gen.routing(3, B, N, L, E, K)
+    g = ev.evict_select_build_union(T(P), T(Q), T(cost), T(ids), E, n_nodes=T(n))
+    s, d = ev.evict_batch_stats(g["k_star"], g["e_hat"], g["utility"], g["union_count"],
+                                g["status"], N, n_nodes=T(n))
+    gg = npy(g)
+    so, do = oracle.batch_stats(N, L, gg["k_star"], gg["e_hat"].astype(np.float64),
+                                gg["utility"].astype(np.float64), gg["union_count"],
+                                gg["status"].astype(np.uint32), n_nodes=n)
+    assert (s.cpu().numpy() == so).all()
+    assert np.allclose(d.cpu().numpy(), do, rtol=1e-9)
+    assert so[4] == 1
