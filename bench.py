@@ -272,12 +272,12 @@ def run_native(args, rank, world, local_rank):
 
     import gen
     import paper_2605_00342_b200 as ev
+    from paper_2605_00342_b200.dist import allreduce_stats, max_over_ranks, shard
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     ev.lib()
-    M = args.trees
-    base = rank * M
+    base, M = shard(rank, world, args.trees)
     # ---- device-resident synthetic inputs (generation excluded from timing)
     P, Q, n = gen.trees_cuda(SEED, M, N_NODES, STEPS, TOPK, tree_base=base)
     cost = torch.from_numpy(gen.cost_table(N_NODES)).to(dev)
@@ -311,9 +311,7 @@ def run_native(args, rank, world, local_rank):
         if ev1 is not None:
             ev1.record(stream)
         stats_call()
-        if world > 1:
-            dist.all_reduce(stats_t)
-            dist.all_reduce(dstats_t)
+        allreduce_stats(stats_t, dstats_t)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -339,9 +337,7 @@ def run_native(args, rank, world, local_rank):
     clocks = clk.stop()
     elapsed_ms = t0.elapsed_time(t1)
     kern_ms = sum(a.elapsed_time(b) for a, b in evs) / K
-    tm = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    tm = max_over_ranks(torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev))
     elapsed_ms, kern_ms = float(tm[0]), float(tm[1])
     st = stats_t.cpu().numpy()
     # single-rank stats of this shard (the all-reduced vector sums every rank)

@@ -94,7 +94,7 @@ def compare_build(o, g):
             i = int(np.argmax(a != b_))
             msgs.append(f"{f} differs at row {i}: oracle {a[i]} gpu {b_[i]}")
     tm_o = np.asarray(o["tree_mask"])[:T]
-    tm_g = _u64(g["tree_mask"]).reshape(tm_o.shape[0] if T else 0, -1)[:T] if T else tm_o
+    tm_g = _u64(g["tree_mask"]).reshape(-1, tm_o.shape[1])[:T]
     if T and not (tm_o == tm_g).all():
         msgs.append("tree_mask differs")
     if "status" in g and not (np.asarray(o["status"]) == np.asarray(g["status"]).astype(np.uint32)).all():

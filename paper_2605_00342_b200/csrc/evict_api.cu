@@ -168,8 +168,8 @@ evict_status_t evict_select_build_union(const evict_trees_t *trees, const float 
     }
     if (!dev_info().ok) return EVICT_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
-    const int ntiles = (trees->batch + kTileTrees - 1) / kTileTrees;
-    if (cudaMemsetAsync(workspace, 0, evict_workspace_bytes(trees->batch), s) != cudaSuccess)
+    const int ntiles = (trees->batch + kFusedTileTrees - 1) / kFusedTileTrees;
+    if (cudaMemsetAsync(workspace, 0, 8 * (1 + (size_t)ntiles), s) != cudaSuccess)
         return EVICT_ERR_CUDA;
     uint64_t *ws = (uint64_t *)workspace;
     if (wide(trees->max_nodes)) return launch_fused<4>(trees, cost, (int)cost_stride, rt, out, ws, ntiles, s);

@@ -28,45 +28,74 @@ constexpr uint64_t kAgg = 1ull << 62;
 constexpr uint64_t kInc = 2ull << 62;
 constexpr uint64_t kValMask = (1ull << 62) - 1;
 
+// The tile state word carries its own payload (flag + count in one aligned
+// 64-bit word), so relaxed GPU-scope accesses suffice: no acquire (which would
+// invalidate L1) and no release fence.
 __device__ __forceinline__ uint64_t ld_acquire(const uint64_t *p)
 {
     uint64_t v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release(uint64_t *p, uint64_t v)
 {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Called by all threads of the CTA after every warp stored its tree's row
-// count in s_cnt[warp].  Returns (in s_off[warp]) the packed-row offset of
-// each warp's tree.  Thread 0 publishes and looks back.
-__device__ __forceinline__ void tile_scan(int tile, uint64_t *states, int *s_cnt, int *s_off)
+// Decoupled look-back over CTA tiles (8 trees each), split in two halves so the
+// wait for predecessors overlaps useful work:
+//  tile_publish  — after every warp stored its tree's row count in s_cnt[warp]:
+//                  warp 0 scans the 8 counts and publishes the tile aggregate
+//                  (tile 0 publishes its inclusive prefix directly).
+//  tile_lookback — later: warp 0 walks back over 32 predecessor states per
+//                  L2 round trip; the nearest inclusive prefix ends the walk,
+//                  unpublished predecessors in front of it are re-polled.
+// s_off[warp] = packed-row offset of the warp's tree after tile_lookback.
+__device__ __forceinline__ void tile_publish(int tile, uint64_t *states, const int *s_cnt, int *s_off,
+                                             int *s_agg)
 {
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int agg = 0;
-        for (int w = 0; w < kWarps; w++) {
-            s_off[w] = agg;
-            agg += s_cnt[w];
+    if ((threadIdx.x >> 5) == 0) {
+        const int lane = lane_id();
+        const int c = lane < kWarps ? s_cnt[lane] : 0;
+        int inc = c;
+#pragma unroll
+        for (int o = 1; o < kWarps; o <<= 1) {
+            int v = __shfl_up_sync(kFull, inc, o);
+            if (lane >= o) inc += v;
         }
-        uint64_t prefix = 0;
-        if (tile == 0) {
-            st_release(states + tile, kInc | (uint64_t)agg);
-        } else {
-            st_release(states + tile, kAgg | (uint64_t)agg);
-            int j = tile - 1;
-            while (true) {
-                uint64_t s = ld_acquire(states + j);
-                if ((s >> 62) == 0) continue;           // predecessor not published yet
-                prefix += s & kValMask;
-                if ((s >> 62) == 2) break;
-                j--;
-            }
-            st_release(states + tile, kInc | (prefix + (uint64_t)agg));
+        const int agg = __shfl_sync(kFull, inc, kWarps - 1);
+        if (lane < kWarps) s_off[lane] = inc - c;
+        if (lane == 0) {
+            *s_agg = agg;
+            st_release(states + tile, (tile == 0 ? kInc : kAgg) | (uint64_t)agg);
         }
-        for (int w = 0; w < kWarps; w++) s_off[w] += (int)prefix;
+    }
+}
+
+__device__ __forceinline__ void tile_lookback(int tile, uint64_t *states, int *s_off, const int *s_agg)
+{
+    __syncthreads();
+    if ((threadIdx.x >> 5) == 0 && tile > 0) {
+        const int lane = lane_id();
+        unsigned prefix = 0;
+        int end = tile;
+        while (true) {
+            const int j = end - 1 - lane;          // lane 0 = nearest predecessor
+            const uint64_t s = j >= 0 ? ld_acquire(states + j) : kInc;
+            const unsigned flag = (unsigned)(s >> 62);
+            const unsigned inc_mask = __ballot_sync(kFull, flag == 2);
+            const unsigned zero_mask = __ballot_sync(kFull, flag == 0);
+            const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
+            const unsigned before = first_inc == 32 ? kFull : ((1u << first_inc) - 1u);
+            if (zero_mask & before) continue;      // a predecessor is not published yet
+            const unsigned v = lane <= first_inc ? (unsigned)(s & kValMask) : 0u;
+            prefix += __reduce_add_sync(kFull, v);
+            if (first_inc < 32) break;
+            end -= 32;
+        }
+        if (lane == 0) st_release(states + tile, kInc | (uint64_t)(prefix + (unsigned)*s_agg));
+        if (lane < kWarps) s_off[lane] += (int)prefix;
     }
     __syncthreads();
 }
@@ -132,7 +161,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_build(evict_trees_t tr, const u
                                                        uint64_t *ws, int ntiles)
 {
     __shared__ WarpSlab<NPL> slab[kWarps];
-    __shared__ int s_cnt[kWarps], s_off[kWarps], s_tile;
+    __shared__ int s_cnt[kWarps], s_off[kWarps], s_tile, s_agg;
     constexpr int W = Shape<NPL>::W;
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int N = tr.max_nodes;
@@ -158,7 +187,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_build(evict_trees_t tr, const u
             }
         }
         if (lane == 0) s_cnt[warp] = k;
-        tile_scan(tile, states, s_cnt, s_off);
+        tile_publish(tile, states, s_cnt, s_off, &s_agg);
+        tile_lookback(tile, states, s_off, &s_agg);
         if (b < tr.batch) {
             const int off = s_off[warp];
             if (lane == 0) {
@@ -188,15 +218,26 @@ __device__ __forceinline__ void tree_fill_klist(const TreeState<NPL> &t, WarpSla
     __syncwarp();
 }
 
+// Flag bytes per warp for the shared-memory union (IDF 1/4): L × Epad.
+__host__ __device__ inline int union_epad(int E) { return E <= 128 ? 128 : 256; }
+
 template <int NPL, int IDF, int KT, int EW, int CL>
 __global__ void __launch_bounds__(kWarps * 32) k_union(evict_trees_t tr, const uint64_t *keep_bits,
                                                        evict_routing_t rt, int32_t *union_count,
                                                        int32_t *union_total, uint64_t *union_bits,
                                                        int64_t *expert_hist, uint32_t *status)
 {
+    extern __shared__ __align__(16) uint8_t dsm[];
     __shared__ WarpSlab<NPL> slab[kWarps];
     constexpr int W = Shape<NPL>::W;
     const int warp = threadIdx.x >> 5, lane = lane_id();
+    const int Epad = union_epad(rt.num_experts);
+    uint8_t *flags = dsm + (size_t)warp * rt.num_layers * Epad;
+    if constexpr (IDF == 1 || IDF == 4) {
+        uint4 *f4 = reinterpret_cast<uint4 *>(flags);
+        for (int i = lane; i < rt.num_layers * Epad / 16; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
+    }
     const int b = blockIdx.x * kWarps + warp;
     if (b >= tr.batch) return;
     const int N = tr.max_nodes;
@@ -219,77 +260,210 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(evict_trees_t tr, const u
     if (!t.status) tree_fill_klist<NPL>(t, sm);
     uint32_t st = t.status;
     tree_union<NPL, IDF, KT, EW, CL>(st, sm, k, b, N, rt.num_layers, rt.top_k, rt.num_experts,
-                                     rt.id_format, rt.ids, union_count, union_total, union_bits, expert_hist);
+                                     rt.id_format, rt.ids, flags, Epad, union_count, union_total,
+                                     union_bits, expert_hist);
     if (status && lane == 0) status[b] = st;
 }
 
 // ------------------------------------------------------------ fused
+// One CTA tile = 32 consecutive trees, 4 per warp (warp w owns trees w, w+8,
+// w+16, w+24 of the tile), processed in three phases:
+//   A  per tree: A1–A5 select (outputs written), A7 union (outputs written),
+//      and an emit record (parent, depth, keep) parked in shared memory;
+//   B  one barrier: warp 0 scans the 32 row counts, publishes the tile
+//      aggregate, looks back for the tile prefix and fetches the next ticket;
+//   C  per tree: A6 build from the record at the packed offset.
+// Two barriers per 32 trees; union-time variance averages over 4 trees/warp.
+constexpr int kTreesPerWarp = 4;
+constexpr int kTile = kWarps * kTreesPerWarp;
+
+template <int NPL>
+struct EmitRec {
+    static constexpr int NMAX = Shape<NPL>::NMAX;
+    static constexpr int W = Shape<NPL>::W;
+    uint64_t keep[W];
+    int8_t par[NMAX];
+    uint8_t dep[NMAX];
+    int n, k;
+    uint32_t status;
+};
+
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+template <int NPL>
+__host__ __device__ constexpr size_t fused_rec_offset() { return align16(sizeof(WarpSlab<NPL>) * kWarps); }
+template <int NPL>
+__host__ __device__ constexpr size_t fused_flags_offset()
+{
+    return align16(fused_rec_offset<NPL>() + sizeof(EmitRec<NPL>) * kTile);
+}
+
 template <int NPL, int IDF, int KT, int EW, int CL>
-__global__ void __launch_bounds__(kWarps * 32) k_fused(evict_trees_t tr, const float *cost,
+__global__ void __launch_bounds__(kWarps * 32, 2) k_fused(evict_trees_t tr, const float *cost,
                                                        int cost_stride, evict_routing_t rt,
                                                        evict_fused_out_t out, uint64_t *ws,
                                                        int ntiles)
 {
-    __shared__ WarpSlab<NPL> slab[kWarps];
-    __shared__ int s_cnt[kWarps], s_off[kWarps], s_tile;
+    extern __shared__ __align__(16) uint8_t dsm[];
+    // dynamic shared memory: [warp slabs][emit records][union flags]
+    WarpSlab<NPL> *slab = reinterpret_cast<WarpSlab<NPL> *>(dsm);
+    EmitRec<NPL> *rec = reinterpret_cast<EmitRec<NPL> *>(dsm + fused_rec_offset<NPL>());
+    __shared__ int s_cnt[kTile], s_off[kTile], s_tile;
+    constexpr int W = Shape<NPL>::W;
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int N = tr.max_nodes;
     const int WN = (N + 63) / 64;
+    const int base = lane * NPL;
     unsigned *ticket = reinterpret_cast<unsigned *>(ws);
     uint64_t *states = ws + 1;
     WarpSlab<NPL> &sm = slab[warp];
-    constexpr int W = Shape<NPL>::W;
-    while (true) {
-        const int tile = next_tile(ticket, &s_tile);
-        if (tile >= ntiles) break;
-        const int b = tile * kWarps + warp;
-        TreeState<NPL> t;
-        int k = 0;
-        if (b < tr.batch) {
-            tree_load_validate<NPL>(t, tr, tr.parent, tr.q, tr.n_nodes, b, N);
-            float c[NPL];
-            if (!(t.status & EVICT_TREE_BAD_SIZE)) tree_load_cost<NPL>(c, t, cost + (size_t)b * cost_stride);
-            int32_t *orow = out.order ? out.order + (size_t)b * N : nullptr;
-            float *prow = out.prefix_sums ? out.prefix_sums + (size_t)b * N : nullptr;
-            if (!t.status) {
-                tree_levels<NPL, true>(t, sm);
-                tree_rank_argmax<NPL>(t, sm, c, N, orow, prow);
-                k = t.kstar;
-            } else {
-                t.kstar = 0; t.ehat = 0.f; t.util = 0.f;
-#pragma unroll
-                for (int w = 0; w < W; w++) t.keep[w] = 0ull;
-                if (orow)
-                    for (int p = lane; p < N; p += 32) { orow[p] = -1; prow[p] = 0.f; }
-            }
-            if (lane == 0) {
-                if (out.k_star) out.k_star[b] = t.kstar;
-                if (out.e_hat) out.e_hat[b] = t.ehat;
-                if (out.utility) out.utility[b] = t.util;
-            }
-            if (out.keep_bits && lane < WN) out.keep_bits[(size_t)b * WN + lane] = t.keep[lane < W ? lane : 0];
+    const int Epad = union_epad(rt.num_experts);
+    uint8_t *flags = dsm + fused_flags_offset<NPL>() + (size_t)warp * rt.num_layers * Epad;
+    if constexpr (IDF == 1 || IDF == 4) {
+        if (out.union_count) {
+            uint4 *f4 = reinterpret_cast<uint4 *>(flags);
+            for (int i = lane; i < rt.num_layers * Epad / 16; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
+            __syncwarp();
         }
-        if (lane == 0) s_cnt[warp] = k;
-        tile_scan(tile, states, s_cnt, s_off);
-        if (b < tr.batch) {
-            const int off = s_off[warp];
+    }
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+    __syncthreads();
+    int tile = s_tile;
+    while (tile < ntiles) {
+        // ---------------- phase A1: select per tree (+ emit record)
+#pragma unroll 1
+        for (int it = 0; it < kTreesPerWarp; it++) {
+            const int slot = warp + kWarps * it;
+            const int b = tile * kTile + slot;
+            int k = 0;
+            if (b < tr.batch) {
+                TreeState<NPL> t;
+                tree_load_validate<NPL>(t, tr, tr.parent, tr.q, tr.n_nodes, b, N);
+                float c[NPL];
+                if (!(t.status & EVICT_TREE_BAD_SIZE)) tree_load_cost<NPL>(c, t, cost + (size_t)b * cost_stride);
+                int32_t *orow = out.order ? out.order + (size_t)b * N : nullptr;
+                float *prow = out.prefix_sums ? out.prefix_sums + (size_t)b * N : nullptr;
+                if (!t.status) {
+                    tree_levels<NPL, true>(t, sm);
+                    tree_rank_argmax<NPL>(t, sm, c, N, orow, prow);
+                    k = t.kstar;
+                } else {
+                    t.kstar = 0; t.ehat = 0.f; t.util = 0.f;
+#pragma unroll
+                    for (int w = 0; w < W; w++) t.keep[w] = 0ull;
+                    if (orow)
+                        for (int p = lane; p < N; p += 32) { orow[p] = -1; prow[p] = 0.f; }
+                }
+                if (lane == 0) {
+                    if (out.k_star) out.k_star[b] = t.kstar;
+                    if (out.e_hat) out.e_hat[b] = t.ehat;
+                    if (out.utility) out.utility[b] = t.util;
+                }
+                if (out.keep_bits && lane < WN) out.keep_bits[(size_t)b * WN + lane] = t.keep[lane < W ? lane : 0];
+                EmitRec<NPL> &er = rec[slot];
+#pragma unroll
+                for (int r = 0; r < NPL; r++) {
+                    er.par[base + r] = (int8_t)t.par[r];
+                    er.dep[base + r] = (uint8_t)t.dep[r];
+                }
+                if (lane < W) er.keep[lane] = t.keep[lane];
+                if (lane == 0) { er.n = t.n; er.k = k; er.status = t.status; }
+            }
+            if (lane == 0) s_cnt[slot] = k;
+        }
+        // ---------------- tile aggregate published as soon as every tree is selected
+        __syncthreads();
+        int incl = 0;
+        if (warp == 0) {
+            const int c = s_cnt[lane];             // kTile == 32 == warp size
+            incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int v = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += v;
+            }
+            s_off[lane] = incl - c;
+            if (lane == 31) st_release(states + tile, (tile == 0 ? kInc : kAgg) | (uint64_t)incl);
+        }
+        // ---------------- phase A2: expert union per tree (the look-back latency hides here)
+        if (out.union_count) {
+#pragma unroll 1
+            for (int it = 0; it < kTreesPerWarp; it++) {
+                const int slot = warp + kWarps * it;
+                const int b = tile * kTile + slot;
+                if (b >= tr.batch) break;
+                EmitRec<NPL> &er = rec[slot];
+                const int k = er.k;
+                uint32_t st = er.status;
+                TreeState<NPL> t;
+                t.n = er.n;
+#pragma unroll
+                for (int w = 0; w < W; w++) t.keep[w] = er.keep[w];
+                if (k > 0) tree_fill_klist<NPL>(t, sm);
+                tree_union<NPL, IDF, KT, EW, CL>(st, sm, k, b, N, rt.num_layers, rt.top_k,
+                                                 rt.num_experts, rt.id_format, rt.ids, flags, Epad,
+                                                 out.union_count, out.union_total, out.union_bits,
+                                                 out.expert_hist);
+                if (lane == 0) er.status = st;
+            }
+        }
+        // ---------------- look-back for the tile prefix + next ticket
+        if (warp == 0) {
+            const int agg = __shfl_sync(kFull, incl, 31);
+            unsigned prefix = 0;
+            if (tile > 0) {
+                int end = tile;
+                while (true) {
+                    const int j = end - 1 - lane;
+                    const uint64_t sv = j >= 0 ? ld_acquire(states + j) : kInc;
+                    const unsigned flag = (unsigned)(sv >> 62);
+                    const unsigned inc_mask = __ballot_sync(kFull, flag == 2);
+                    const unsigned zero_mask = __ballot_sync(kFull, flag == 0);
+                    const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
+                    const unsigned before = first_inc == 32 ? kFull : ((1u << first_inc) - 1u);
+                    if (zero_mask & before) continue;
+                    const unsigned v = lane <= first_inc ? (unsigned)(sv & kValMask) : 0u;
+                    prefix += __reduce_add_sync(kFull, v);
+                    if (first_inc < 32) break;
+                    end -= 32;
+                }
+                if (lane == 0) st_release(states + tile, kInc | (uint64_t)(prefix + (unsigned)agg));
+            }
+            s_off[lane] += (int)prefix;
+            if (lane == 0) s_tile = (int)atomicAdd(ticket, 1u);
+        }
+        __syncthreads();
+        const int next = s_tile;
+        // ---------------- phase C: verify-tree build per tree
+#pragma unroll 1
+        for (int it = 0; it < kTreesPerWarp; it++) {
+            const int slot = warp + kWarps * it;
+            const int b = tile * kTile + slot;
+            if (b >= tr.batch) break;
+            const EmitRec<NPL> &er = rec[slot];
+            const int k = er.k;
+            const int off = s_off[slot];
+            if (lane == 0 && out.status) out.status[b] = er.status;
             if (lane == 0 && out.verify_offsets) {
                 out.verify_offsets[b] = off;
                 if (b == tr.batch - 1) out.verify_offsets[tr.batch] = off + k;
             }
-            if (k > 0)
+            if (k > 0) {
+                TreeState<NPL> t;
+                t.n = er.n;
+#pragma unroll
+                for (int r = 0; r < NPL; r++) {
+                    t.par[r] = er.par[base + r];
+                    t.dep[r] = er.dep[base + r];
+                }
+#pragma unroll
+                for (int w = 0; w < W; w++) t.keep[w] = er.keep[w];
                 tree_build_emit<NPL>(t, sm, k, b, N, off,
                                      out.pos_offset ? __ldg(out.pos_offset + b) : 0, out.kept_index,
                                      out.retrieve_index, out.positions, out.next_token,
                                      out.next_sibling, out.tree_mask);
-            __syncwarp();
-            uint32_t st = t.status;
-            if (out.union_count)
-                tree_union<NPL, IDF, KT, EW, CL>(st, sm, k, b, N, rt.num_layers, rt.top_k,
-                                                 rt.num_experts, rt.id_format, rt.ids, out.union_count,
-                                                 out.union_total, out.union_bits, out.expert_hist);
-            if (out.status && lane == 0) out.status[b] = st;
+            }
         }
+        tile = next;
     }
 }
 
@@ -299,10 +473,10 @@ int dev_sms();  // evict_api.cu
 inline evict_status_t launched() { return cudaGetLastError() == cudaSuccess ? EVICT_OK : EVICT_ERR_CUDA; }
 
 template <typename K>
-inline int persistent_blocks(K kernel, int ntiles)
+inline int persistent_blocks(K kernel, int ntiles, size_t dyn = 0)
 {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, dyn);
     if (per_sm < 1) per_sm = 1;
     long g = (long)dev_sms() * per_sm;
     return (int)(g < ntiles ? g : ntiles);
@@ -313,20 +487,38 @@ inline int persistent_blocks(K kernel, int ntiles)
 template <int NPL, template <int, int, int, int, int> class Launcher, typename... Args>
 inline evict_status_t dispatch_union(const evict_routing_t *rt, Args... args)
 {
-    const int CL = rt->num_layers <= 64 ? 2 : 4;
+    // Fast slot layout (evict_tree.cuh tree_union_fast) for top-8 ids and 1/2/4-word masks:
+    // L·P slots in R register rounds (R·32 ≥ L·P).  Otherwise the lane-per-layer layout
+    // with R/2 rounds (R/2·32 ≥ L).
+    const int L = rt->num_layers;
+    const int EWr = (rt->num_experts + 63) / 64;
     const int EW = rt->num_experts <= 128 ? 2 : 4;
-#define EVICT_CL(IDF, EWV)                                                    \
-    if (CL == 2) return Launcher<NPL, IDF, IDF == 1 || IDF == 4 ? 8 : 0, EWV, 2>::run(args...); \
-    return Launcher<NPL, IDF, IDF == 1 || IDF == 4 ? 8 : 0, EWV, 4>::run(args...);
-#define EVICT_EW(IDF)                     \
-    if (EW == 2) { EVICT_CL(IDF, 2) }     \
-    else { EVICT_CL(IDF, 4) }
-    if (rt->id_format == EVICT_ID_MASK) { EVICT_EW(8) }
-    if (rt->top_k == 8 && rt->id_format == EVICT_ID_U8) { EVICT_EW(1) }
-    if (rt->top_k == 8 && rt->id_format == EVICT_ID_I32) { EVICT_EW(4) }
-    EVICT_EW(0)
+    int IDF = 0;
+    if (rt->id_format == EVICT_ID_MASK) IDF = (EWr == 3) ? 9 : 8;
+    else if (rt->top_k == 8) IDF = rt->id_format;
+    const int P = IDF == 8 ? EWr : 2;
+    int R = (IDF == 1 || IDF == 4 || IDF == 8) ? (L * P <= 96 ? 3 : (L * P <= 128 ? 4 : 8))
+                                               : (L <= 64 ? 4 : 8);
+    if ((IDF == 1 || IDF == 4 || IDF == 8) && L * P > 256) {
+        if (IDF == 8) IDF = 9; else IDF = 0;
+        R = L <= 64 ? 4 : 8;
+    }
+#define EVICT_R(IDFV, EWV)                                                            \
+    if (R == 3) return Launcher<NPL, IDFV, (IDFV == 1 || IDFV == 4) ? 8 : 0, EWV, 3>::run(args...); \
+    if (R == 4) return Launcher<NPL, IDFV, (IDFV == 1 || IDFV == 4) ? 8 : 0, EWV, 4>::run(args...); \
+    return Launcher<NPL, IDFV, (IDFV == 1 || IDFV == 4) ? 8 : 0, EWV, 8>::run(args...);
+#define EVICT_EW(IDFV)                  \
+    if (EW == 2) { EVICT_R(IDFV, 2) }   \
+    else { EVICT_R(IDFV, 4) }
+    switch (IDF) {
+    case 1: EVICT_EW(1)
+    case 4: EVICT_EW(4)
+    case 8: EVICT_EW(8)
+    case 9: EVICT_EW(9)
+    default: EVICT_EW(0)
+    }
 #undef EVICT_EW
-#undef EVICT_CL
+#undef EVICT_R
 }
 
 template <int NPL, int IDF, int KT, int EW, int CL>
@@ -336,7 +528,10 @@ struct UnionLauncher {
                               cudaStream_t s)
     {
         const int blocks = (tr->batch + kWarps - 1) / kWarps;
-        k_union<NPL, IDF, KT, EW, CL><<<blocks, kWarps * 32, 0, s>>>(*tr, keep, *rt, uc, ut, ub, eh, st);
+        const size_t dyn = (IDF == 1 || IDF == 4) ? (size_t)kWarps * rt->num_layers * union_epad(rt->num_experts) : 0;
+        auto kern = k_union<NPL, IDF, KT, EW, CL>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        kern<<<blocks, kWarps * 32, dyn, s>>>(*tr, keep, *rt, uc, ut, ub, eh, st);
         return launched();
     }
 };
@@ -348,8 +543,12 @@ struct FusedLauncher {
                               int ntiles, cudaStream_t s)
     {
         auto kern = k_fused<NPL, IDF, KT, EW, CL>;
-        const int blocks = persistent_blocks(kern, ntiles);
-        kern<<<blocks, kWarps * 32, 0, s>>>(*tr, cost, cs, *rt, *o, ws, ntiles);
+        const size_t dyn = fused_flags_offset<NPL>() +
+                           ((IDF == 1 || IDF == 4) && o->union_count
+                                ? (size_t)kWarps * rt->num_layers * union_epad(rt->num_experts) : 0);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        const int blocks = persistent_blocks(kern, ntiles, dyn);
+        kern<<<blocks, kWarps * 32, dyn, s>>>(*tr, cost, cs, *rt, *o, ws, ntiles);
         return launched();
     }
 };

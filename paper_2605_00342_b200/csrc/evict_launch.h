@@ -21,7 +21,8 @@
         const evict_fused_out_t *, uint64_t *, int, cudaStream_t
 
 namespace evict {
-constexpr int kTileTrees = 8;  // trees per CTA tile (= kWarps)
+constexpr int kTileTrees = 8;        // trees per CTA tile of k_build (= warps per CTA)
+constexpr int kFusedTileTrees = 32;  // trees per CTA tile of k_fused (4 per warp)
 int dev_sms();
 template <int NPL> evict_status_t launch_select(EVICT_SELECT_ARGS);
 template <int NPL> evict_status_t launch_build(EVICT_BUILD_ARGS);

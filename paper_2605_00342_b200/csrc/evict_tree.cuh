@@ -41,7 +41,7 @@ template <int NPL>
 struct WarpSlab {
     static constexpr int NMAX = Shape<NPL>::NMAX;
     static constexpr int W = Shape<NPL>::W;
-    float score[NMAX];          // A2 parent lookup
+    int2 sd[NMAX];              // A2 (score bits, depth) of the previous sweep
     uint8_t rank[NMAX];         // A3 node → rank
     uint8_t klist[NMAX];        // A7 slot → node
     uint64_t row[NMAX][W];      // A6 mask rows by slot
@@ -169,52 +169,53 @@ __device__ __forceinline__ void tree_load_cost(float (&c)[NPL], TreeState<NPL> &
 }
 
 // ------------------------------------------------------------ A2: path products
-// Level-synchronous: a node takes score[parent]·q once its parent is final,
-// so each Score(v) is the exact serial root→leaf fp32 product (Eq. 7).
-// dep = depth.  With SCORES = false only the depth is computed.
+// Synchronous sweeps: every sweep, every node recomputes (score, depth) from
+// its parent's value of the previous sweep.  After sweep t every node of
+// depth ≤ t holds fl32(Score(parent)·q) computed from its parent's FINAL
+// value, i.e. exactly the serial root→leaf product of Eq. 7 (deeper nodes
+// hold scratch that later sweeps overwrite).  The loop ends on the first
+// sweep that changes nothing: depth+2 sweeps, branch-free per node.
+// With SCORES = false only the depth is computed.
 template <int NPL, bool SCORES>
 __device__ __forceinline__ void tree_levels(TreeState<NPL> &t, WarpSlab<NPL> &sm)
 {
     const int base = lane_id() * NPL;
-    bool done[NPL];
+    bool live[NPL];
+    int pidx[NPL];
 #pragma unroll
     for (int r = 0; r < NPL; r++) {
         const int i = base + r;
-        done[r] = (i == 0) || (i >= t.n);
-        t.sc[r] = (i == 0) ? 1.f : 0.f;
+        live[r] = (i > 0) && (i < t.n);
+        pidx[r] = live[r] ? t.par[r] : 0;
+        t.sc[r] = 1.f;
         t.dep[r] = 0;
-        sm.score[i] = (i == 0) ? 1.f : -1.f;
+        sm.sd[i] = make_int2(__float_as_int(1.f), 0);
     }
     __syncwarp();
-    for (int it = 1;; it++) {
-        bool pending = false;
-        bool fresh[NPL];
+    while (true) {
+        bool changed = false;
+        float ns[NPL];
+        int nd[NPL];
 #pragma unroll
         for (int r = 0; r < NPL; r++) {
-            fresh[r] = false;
-            if (!done[r]) {
-                float ps = sm.score[t.par[r]];
-                if (ps >= 0.f) {
-                    if constexpr (SCORES) {
-                        float s = __fmul_rn(ps, t.q[r]);
-                        t.sc[r] = (s == 0.f) ? 0.f : s;
-                    }
-                    t.dep[r] = it;
-                    fresh[r] = true;
-                } else {
-                    pending = true;
-                }
+            const int2 pv = sm.sd[pidx[r]];
+            float sv = t.sc[r];
+            if constexpr (SCORES) {
+                sv = __fmul_rn(__int_as_float(pv.x), t.q[r]);   // both ≥ +0: never -0
             }
+            ns[r] = live[r] ? sv : t.sc[r];
+            nd[r] = live[r] ? pv.y + 1 : t.dep[r];
+            changed |= (__float_as_int(ns[r]) != __float_as_int(t.sc[r])) | (nd[r] != t.dep[r]);
         }
         __syncwarp();
 #pragma unroll
-        for (int r = 0; r < NPL; r++)
-            if (fresh[r]) {
-                sm.score[base + r] = SCORES ? t.sc[r] : 0.f;
-                done[r] = true;
-            }
+        for (int r = 0; r < NPL; r++) {
+            t.sc[r] = ns[r];
+            t.dep[r] = nd[r];
+            sm.sd[base + r] = make_int2(__float_as_int(ns[r]), nd[r]);
+        }
         __syncwarp();
-        if (!__any_sync(kFull, pending)) break;
+        if (!__any_sync(kFull, changed)) break;
     }
 }
 
@@ -464,22 +465,50 @@ __device__ __forceinline__ void tree_build_emit(const TreeState<NPL> &t, WarpSla
 // per-layer EW-word expert bitsets; counts are __popcll of the bitsets.
 template <int EW>
 struct LayerBits {
-    uint64_t w[EW];
+    uint32_t w[2 * EW];  // 32-bit words: expert e ⇔ bit e%32 of word e/32
 };
 
+// 1 << s with PTX clamp semantics: 0 for any s ≥ 32 (s is unsigned, so a
+// "negative" s - 32j also gives 0).  One SHF per call.
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t s)
+{
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(1u), "r"(s));
+    return r;
+}
+
+// OR expert e into the layer's bitset: word j gets 1 << (e - 32j), which is
+// non-zero only for the one word that holds e (no per-word compare/select).
 template <int EW>
 __device__ __forceinline__ void or_id(LayerBits<EW> &bs, uint32_t e, uint32_t &bad, uint32_t E)
 {
     bad |= (e >= E);
-    const uint64_t x = 1ull << (e & 63);
 #pragma unroll
-    for (int w = 0; w < EW; w++)
-        if ((e >> 6) == (uint32_t)w) bs.w[w] |= x;
+    for (int j = 0; j < 2 * EW; j++) bs.w[j] |= shl_clamp(e - 32u * j);
+}
+
+// Four u8 ids packed in one word (E == 128 fast path: the id is bad iff bit 7 is set).
+template <int EW>
+__device__ __forceinline__ void or_ids_u8x4(LayerBits<EW> &bs, uint32_t wv, uint32_t &bad, uint32_t E)
+{
+    if (E == 128) {
+        bad |= wv & 0x80808080u;
+    } else {
+#pragma unroll
+        for (int s = 0; s < 4; s++) bad |= (__byte_perm(wv, 0, 0x4440 | s) >= E);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; s++) {
+        const uint32_t e = __byte_perm(wv, 0, 0x4440 | s);
+#pragma unroll
+        for (int j = 0; j < 2 * EW; j++) bs.w[j] |= shl_clamp(e - 32u * j);
+    }
 }
 
 // IDF: 1 = u8 ids, 4 = i32 ids, 8 = masks.  KT: compile-time K (0 = runtime).
+// Generic layout: lane `lane` owns layers l = lane + 32c (any K, any E ≤ 256).
 template <int NPL, int IDF, int KT, int EW, int CL>
-__device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL> &sm, int k,
+__device__ __forceinline__ void tree_union_generic(uint32_t &status, const WarpSlab<NPL> &sm, int k,
                                            int b, int N, int L, int K, int E, int idb,
                                            const void *__restrict__ ids,
                                            int32_t *__restrict__ union_count,
@@ -492,7 +521,7 @@ __device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL>
 #pragma unroll
     for (int c = 0; c < CL; c++)
 #pragma unroll
-        for (int w = 0; w < EW; w++) bs[c].w[w] = 0ull;
+        for (int w = 0; w < 2 * EW; w++) bs[c].w[w] = 0u;
     uint32_t bad = 0;
     const int Kr = KT ? KT : K;
     if (!status) {
@@ -518,11 +547,8 @@ __device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL>
                     for (int c = 0; c < CL; c++) {
                         if (j0 + u >= k || lane + 32 * c >= L) continue;
 #pragma unroll
-                        for (int h = 0; h < 2; h++) {
-                            const uint32_t wv = h ? v[u][c].y : v[u][c].x;
-#pragma unroll
-                            for (int s = 0; s < 4; s++) or_id<EW>(bs[c], (wv >> (8 * s)) & 0xffu, bad, E);
-                        }
+                        or_ids_u8x4<EW>(bs[c], v[u][c].x, bad, E);
+                        or_ids_u8x4<EW>(bs[c], v[u][c].y, bad, E);
                     }
             } else if constexpr (IDF == 4 && KT == 8) {
                 int4 v[U][CL][2];
@@ -554,25 +580,27 @@ __device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL>
                             or_id<EW>(bs[c], (uint32_t)v[u][c][h].w, bad, E);
                         }
                     }
-            } else if constexpr (IDF == 8) {
+            } else if constexpr (IDF >= 8) {
+                const int EWr = (E + 63) >> 6;   // row stride in 64-bit words
                 uint64_t v[U][CL][EW];
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int j = j0 + u;
                     const int node = j < k ? sm.klist[j] : 0;
-                    const uint64_t *rowp = (const uint64_t *)ids + ((size_t)b * N + node) * L * EW;
+                    const uint64_t *rowp = (const uint64_t *)ids + ((size_t)b * N + node) * L * EWr;
 #pragma unroll
                     for (int c = 0; c < CL; c++) {
                         const int l = lane + 32 * c;
                         const bool ok = j < k && l < L;
-                        if constexpr (EW == 2) {
+                        if (EW == 2 && EWr == 2) {
                             ulonglong2 x = ok ? __ldg(reinterpret_cast<const ulonglong2 *>(rowp + l * 2))
                                               : make_ulonglong2(0, 0);
                             v[u][c][0] = x.x;
                             v[u][c][1] = x.y;
                         } else {
 #pragma unroll
-                            for (int w = 0; w < EW; w++) v[u][c][w] = ok ? __ldg(rowp + l * EW + w) : 0ull;
+                            for (int w = 0; w < EW; w++)
+                                v[u][c][w] = (ok && w < EWr) ? __ldg(rowp + l * EWr + w) : 0ull;
                         }
                     }
                 }
@@ -581,7 +609,10 @@ __device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL>
 #pragma unroll
                     for (int c = 0; c < CL; c++)
 #pragma unroll
-                        for (int w = 0; w < EW; w++) bs[c].w[w] |= v[u][c][w];
+                        for (int w = 0; w < EW; w++) {
+                            bs[c].w[2 * w] |= (uint32_t)v[u][c][w];
+                            bs[c].w[2 * w + 1] |= (uint32_t)(v[u][c][w] >> 32);
+                        }
             } else {
                 // generic K (any ≤ 16), u8 or i32: scalar loads
 #pragma unroll 1
@@ -603,14 +634,14 @@ __device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL>
                 }
             }
         }
-        if constexpr (IDF == 8) {
+        if constexpr (IDF >= 8) {
             // bits at or above E are not experts
 #pragma unroll
             for (int c = 0; c < CL; c++)
 #pragma unroll
-                for (int w = 0; w < EW; w++) {
-                    const int lo = w * 64;
-                    uint64_t valid = E >= lo + 64 ? ~0ull : (E <= lo ? 0ull : ((1ull << (E - lo)) - 1ull));
+                for (int w = 0; w < 2 * EW; w++) {
+                    const int lo = w * 32;
+                    uint32_t valid = E >= lo + 32 ? ~0u : (E <= lo ? 0u : ((1u << (E - lo)) - 1u));
                     if (bs[c].w[w] & ~valid) bad = 1;
                 }
         }
@@ -624,9 +655,9 @@ __device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL>
         if (l >= L) continue;
         int cnt = 0;
 #pragma unroll
-        for (int w = 0; w < EW; w++) {
-            if (zero) bs[c].w[w] = 0ull;
-            cnt += __popcll(bs[c].w[w]);
+        for (int w = 0; w < 2 * EW; w++) {
+            if (zero) bs[c].w[w] = 0u;
+            cnt += __popc(bs[c].w[w]);
         }
         tot += cnt;
         union_count[(size_t)b * L + l] = cnt;
@@ -634,14 +665,16 @@ __device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL>
         if (union_bits) {
 #pragma unroll
             for (int w = 0; w < EW; w++)
-                if (w < EWr) union_bits[((size_t)b * L + l) * EWr + w] = bs[c].w[w];
+                if (w < EWr)
+                    union_bits[((size_t)b * L + l) * EWr + w] =
+                        (uint64_t)bs[c].w[2 * w] | ((uint64_t)bs[c].w[2 * w + 1] << 32);
         }
         if (expert_hist && !zero) {
 #pragma unroll
-            for (int w = 0; w < EW; w++) {
-                uint64_t m = bs[c].w[w];
+            for (int w = 0; w < 2 * EW; w++) {
+                uint32_t m = bs[c].w[w];
                 while (m) {
-                    const int e = w * 64 + __ffsll((long long)m) - 1;
+                    const int e = w * 32 + __ffs(m) - 1;
                     m &= m - 1;
                     atomicAdd(reinterpret_cast<unsigned long long *>(expert_hist + (size_t)l * E + e), 1ull);
                 }
@@ -650,6 +683,369 @@ __device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL>
     }
     tot = __reduce_add_sync(kFull, tot);
     if (union_total && lane == 0) union_total[b] = tot;
+}
+
+}  // namespace evict
+
+namespace evict {
+
+// Fast layout: a layer's routing row splits into P parts (4 ids = half of a
+// top-8 row, or one 64-bit mask word); slot = l·P + part is owned by lane
+// slot % 32 in round slot / 32, so every load instruction of the warp reads
+// 32 consecutive parts (128 B of u8 ids, 512 B of i32 ids, 256 B of masks) and
+// no lane idles.  Parts of one layer sit in adjacent lanes and are merged with
+// __shfl_xor_sync at the end.  R = register rounds (≥ ceil(L·P/32)).
+template <int NPL, int IDF, int EW, int R>
+__device__ __forceinline__ void tree_union_fast(uint32_t &status, const WarpSlab<NPL> &sm, int k,
+                                                int b, int N, int L, int E,
+                                                const void *__restrict__ ids,
+                                                int32_t *__restrict__ union_count,
+                                                int32_t *__restrict__ union_total,
+                                                uint64_t *__restrict__ union_bits,
+                                                int64_t *__restrict__ expert_hist)
+{
+    constexpr bool MASK = IDF == 8;
+    constexpr int NW = MASK ? 2 : 2 * EW;      // 32-bit words held per slot
+    const int lane = lane_id();
+    const int EWr = (E + 63) >> 6;
+    const int P = MASK ? EWr : 2;              // parts per layer (1, 2 or 4)
+    const int S = L * P;                       // slots
+    uint32_t bs[R][NW];
+#pragma unroll
+    for (int c = 0; c < R; c++)
+#pragma unroll
+        for (int w = 0; w < NW; w++) bs[c][w] = 0u;
+    uint32_t bad = 0;
+    if (!status) {
+        // bytes per node row: u8 L·8, i32 L·32, mask L·EWr·8
+        const size_t row_elems = MASK ? (size_t)S : (size_t)L * 8;
+        constexpr int U = 4;                    // node rows in flight
+        for (int j0 = 0; j0 < k; j0 += U) {
+            if constexpr (IDF == 1) {
+                uint32_t v[U][R];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int j = j0 + u;
+                    const uint32_t *rowp = reinterpret_cast<const uint32_t *>(
+                        (const uint8_t *)ids + ((size_t)b * N + (j < k ? sm.klist[j] : 0)) * row_elems);
+#pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        const int sl = lane + 32 * c;
+                        v[u][c] = (j < k && sl < S) ? __ldg(rowp + sl) : 0u;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int c = 0; c < R; c++)
+                        if (j0 + u < k && lane + 32 * c < S) {
+                            LayerBits<EW> lb;
+#pragma unroll
+                            for (int w = 0; w < NW; w++) lb.w[w] = bs[c][w];
+                            or_ids_u8x4<EW>(lb, v[u][c], bad, E);
+#pragma unroll
+                            for (int w = 0; w < NW; w++) bs[c][w] = lb.w[w];
+                        }
+            } else if constexpr (IDF == 4) {
+                int4 v[U][R];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int j = j0 + u;
+                    const int4 *rowp = reinterpret_cast<const int4 *>(
+                        (const int32_t *)ids + ((size_t)b * N + (j < k ? sm.klist[j] : 0)) * row_elems);
+#pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        const int sl = lane + 32 * c;
+                        v[u][c] = (j < k && sl < S) ? __ldg(rowp + sl) : make_int4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int c = 0; c < R; c++)
+                        if (j0 + u < k && lane + 32 * c < S) {
+                            LayerBits<EW> lb;
+#pragma unroll
+                            for (int w = 0; w < NW; w++) lb.w[w] = bs[c][w];
+                            or_id<EW>(lb, (uint32_t)v[u][c].x, bad, E);
+                            or_id<EW>(lb, (uint32_t)v[u][c].y, bad, E);
+                            or_id<EW>(lb, (uint32_t)v[u][c].z, bad, E);
+                            or_id<EW>(lb, (uint32_t)v[u][c].w, bad, E);
+#pragma unroll
+                            for (int w = 0; w < NW; w++) bs[c][w] = lb.w[w];
+                        }
+            } else {
+                uint2 v[U][R];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int j = j0 + u;
+                    const uint2 *rowp = reinterpret_cast<const uint2 *>(
+                        (const uint64_t *)ids + ((size_t)b * N + (j < k ? sm.klist[j] : 0)) * row_elems);
+#pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        const int sl = lane + 32 * c;
+                        v[u][c] = (j < k && sl < S) ? __ldg(rowp + sl) : make_uint2(0u, 0u);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        bs[c][0] |= v[u][c].x;
+                        bs[c][1] |= v[u][c].y;
+                    }
+            }
+        }
+        if constexpr (MASK) {
+            if (E & 63) {   // bits at or above E are not experts
+#pragma unroll
+                for (int c = 0; c < R; c++) {
+                    const int sl = lane + 32 * c;
+                    if (sl < S && (sl % P) == P - 1) {
+                        const int lo = (P - 1) * 64, rem = E - lo;
+                        const uint64_t m = (uint64_t)bs[c][0] | ((uint64_t)bs[c][1] << 32);
+                        if (m & ~((1ull << rem) - 1ull)) bad = 1;
+                    }
+                }
+            }
+        }
+        if (__any_sync(kFull, bad)) status |= EVICT_TREE_BAD_EXPERT;
+    }
+    const bool zero = status != 0;
+    int tot = 0;
+#pragma unroll
+    for (int c = 0; c < R; c++) {
+        const int sl = lane + 32 * c;
+        const int l = sl / P, h = sl - l * P;
+        if (zero) {
+#pragma unroll
+            for (int w = 0; w < NW; w++) bs[c][w] = 0u;
+        }
+        int cnt;
+        if constexpr (!MASK) {
+            // merge the two halves of the layer (adjacent lanes)
+#pragma unroll
+            for (int w = 0; w < NW; w++) bs[c][w] |= __shfl_xor_sync(kFull, bs[c][w], 1);
+            cnt = 0;
+#pragma unroll
+            for (int w = 0; w < NW; w++) cnt += __popc(bs[c][w]);
+        } else {
+            cnt = __popc(bs[c][0]) + __popc(bs[c][1]);
+            if (P >= 2) cnt += __shfl_xor_sync(kFull, cnt, 1);
+            if (P >= 4) cnt += __shfl_xor_sync(kFull, cnt, 2);
+        }
+        if (sl >= S) continue;
+        if (h == 0) {
+            union_count[(size_t)b * L + l] = cnt;
+            tot += cnt;
+        }
+        // this lane owns 64-bit words w with w % P == h (ids: of the merged set)
+        uint64_t *dst = union_bits ? union_bits + ((size_t)b * L + l) * EWr : nullptr;
+        if constexpr (!MASK) {
+#pragma unroll
+            for (int w = 0; w < EW; w++) {
+                if (w < EWr && (w & 1) == h) {
+                    const uint64_t m = (uint64_t)bs[c][2 * w] | ((uint64_t)bs[c][2 * w + 1] << 32);
+                    if (dst) dst[w] = m;
+                    if (expert_hist && !zero) {
+                        uint64_t mm = m;
+                        while (mm) {
+                            const int e = w * 64 + __ffsll((long long)mm) - 1;
+                            mm &= mm - 1;
+                            atomicAdd(reinterpret_cast<unsigned long long *>(expert_hist + (size_t)l * E + e), 1ull);
+                        }
+                    }
+                }
+            }
+        } else {
+            const uint64_t m = (uint64_t)bs[c][0] | ((uint64_t)bs[c][1] << 32);
+            if (dst) dst[h] = m;
+            if (expert_hist && !zero) {
+                uint64_t mm = m;
+                while (mm) {
+                    const int e = h * 64 + __ffsll((long long)mm) - 1;
+                    mm &= mm - 1;
+                    atomicAdd(reinterpret_cast<unsigned long long *>(expert_hist + (size_t)l * E + e), 1ull);
+                }
+            }
+        }
+    }
+    tot = __reduce_add_sync(kFull, tot);
+    if (union_total && lane == 0) union_total[b] = tot;
+}
+
+// Top-8 ids (u8 or i32) via per-warp shared-memory expert flags: the union of
+// a layer is the set of flag bytes written.  Each id costs one byte store
+// (a warp store covers 32 ids, no read-modify-write, duplicate ids are
+// idempotent), instead of building one-hot words in registers.  The flag
+// region of the warp is [L][Epad] bytes (Epad = E rounded up to 128); a layer
+// splits into two halves owned by adjacent lanes (slot = 2l + half), which
+// count (popc of 0/1 bytes), optionally pack bits, and clear their half.
+template <int NPL, int IDF, int R>
+__device__ __forceinline__ void tree_union_flags(uint32_t &status, const WarpSlab<NPL> &sm, int k,
+                                                 int b, int N, int L, int E,
+                                                 const void *__restrict__ ids, uint8_t *flags,
+                                                 int Epad, int32_t *__restrict__ union_count,
+                                                 int32_t *__restrict__ union_total,
+                                                 uint64_t *__restrict__ union_bits,
+                                                 int64_t *__restrict__ expert_hist)
+{
+    const int lane = lane_id();
+    const int S = 2 * L;
+    uint32_t bad = 0;
+    if (!status) {
+        const size_t row = (size_t)L * 8;                  // ids per node row
+        const uint8_t *tree_u8 = (const uint8_t *)ids + (size_t)b * N * row;
+        const int32_t *tree_i32 = (const int32_t *)ids + (size_t)b * N * row;
+        constexpr int U = 4;
+        for (int j0 = 0; j0 < k; j0 += U) {
+            if constexpr (IDF == 1) {
+                uint32_t v[U][R];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int j = j0 + u;
+                    const uint32_t *rowp = reinterpret_cast<const uint32_t *>(
+                        tree_u8 + (uint32_t)(j < k ? sm.klist[j] : 0) * (uint32_t)row);
+#pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        const int sl = lane + 32 * c;
+                        v[u][c] = (j < k && sl < S) ? __ldg(rowp + sl) : 0u;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        const int sl = lane + 32 * c;
+                        if (j0 + u < k && sl < S) {
+                            uint8_t *fl = flags + (sl >> 1) * Epad;
+                            const uint32_t wv = v[u][c];
+                            if (E == 128) {
+                                bad |= wv & 0x80808080u;
+#pragma unroll
+                                for (int q = 0; q < 4; q++) fl[__byte_perm(wv, 0, 0x4440 | q) & 127u] = 1;
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < 4; q++) {
+                                    const uint32_t e = __byte_perm(wv, 0, 0x4440 | q);
+                                    if (e < (uint32_t)E) fl[e] = 1; else bad = 1;
+                                }
+                            }
+                        }
+                    }
+            } else {
+                int4 v[U][R];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int j = j0 + u;
+                    const int4 *rowp = reinterpret_cast<const int4 *>(
+                        tree_i32 + (uint32_t)(j < k ? sm.klist[j] : 0) * (uint32_t)row);
+#pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        const int sl = lane + 32 * c;
+                        v[u][c] = (j < k && sl < S) ? __ldg(rowp + sl) : make_int4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        const int sl = lane + 32 * c;
+                        if (j0 + u < k && sl < S) {
+                            uint8_t *fl = flags + (sl >> 1) * Epad;
+                            const uint32_t e4[4] = {(uint32_t)v[u][c].x, (uint32_t)v[u][c].y,
+                                                    (uint32_t)v[u][c].z, (uint32_t)v[u][c].w};
+#pragma unroll
+                            for (int q = 0; q < 4; q++) {
+                                if (e4[q] < (uint32_t)E) fl[e4[q]] = 1; else bad = 1;
+                            }
+                        }
+                    }
+            }
+        }
+        if (__any_sync(kFull, bad)) status |= EVICT_TREE_BAD_EXPERT;
+    }
+    __syncwarp();
+    const bool zero = status != 0;
+    const bool want_bits = union_bits != nullptr || expert_hist != nullptr;
+    const int half = Epad >> 1;                       // bytes (= experts) per half, multiple of 64
+    const int EWr = (E + 63) >> 6;
+    int tot = 0;
+#pragma unroll
+    for (int c = 0; c < R; c++) {
+        const int sl = lane + 32 * c;
+        const bool in = sl < S;
+        const int l = sl >> 1, h = sl & 1;
+        int cnt = 0;
+        uint64_t bits[2] = {0ull, 0ull};              // half ≤ 128 experts
+        if (in) {
+            uint4 *fp = reinterpret_cast<uint4 *>(flags + l * Epad + h * half);
+            for (int q = 0; q < (half >> 4); q++) {
+                const uint4 x = fp[q];
+                cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+                if (want_bits) {
+                    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                    for (int m = 0; m < 4; m++) {
+                        const uint32_t nib = (xs[m] & 1u) | ((xs[m] >> 7) & 2u) | ((xs[m] >> 14) & 4u) |
+                                             ((xs[m] >> 21) & 8u);
+                        const int pos = q * 16 + m * 4;
+                        bits[pos >> 6] |= (uint64_t)nib << (pos & 63);
+                    }
+                }
+                fp[q] = make_uint4(0u, 0u, 0u, 0u);
+            }
+        }
+        cnt += __shfl_xor_sync(kFull, cnt, 1);
+        if (zero) {
+            cnt = 0;
+            bits[0] = bits[1] = 0ull;
+        }
+        if (!in) continue;
+        if (h == 0) {
+            union_count[(size_t)b * L + l] = cnt;
+            tot += cnt;
+        }
+        const int w0 = h * (half >> 6);               // first 64-bit word of this half
+#pragma unroll
+        for (int w = 0; w < 2; w++) {
+            if (w < (half >> 6) && w0 + w < EWr) {
+                if (union_bits) union_bits[((size_t)b * L + l) * EWr + w0 + w] = bits[w];
+                if (expert_hist && !zero) {
+                    uint64_t mm = bits[w];
+                    while (mm) {
+                        const int e = (w0 + w) * 64 + __ffsll((long long)mm) - 1;
+                        mm &= mm - 1;
+                        atomicAdd(reinterpret_cast<unsigned long long *>(expert_hist + (size_t)l * E + e), 1ull);
+                    }
+                }
+            }
+        }
+    }
+    __syncwarp();
+    tot = __reduce_add_sync(kFull, tot);
+    if (union_total && lane == 0) union_total[b] = tot;
+}
+
+// Dispatch: flags for top-8 ids, register OR for 1/2/4-word masks, generic otherwise.
+template <int NPL, int IDF, int KT, int EW, int R>
+__device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL> &sm, int k, int b,
+                                           int N, int L, int K, int E, int idb,
+                                           const void *__restrict__ ids, uint8_t *flags, int Epad,
+                                           int32_t *__restrict__ union_count,
+                                           int32_t *__restrict__ union_total,
+                                           uint64_t *__restrict__ union_bits,
+                                           int64_t *__restrict__ expert_hist)
+{
+    if constexpr (IDF == 1 || IDF == 4)
+        tree_union_flags<NPL, IDF, R>(status, sm, k, b, N, L, E, ids, flags, Epad, union_count,
+                                      union_total, union_bits, expert_hist);
+    else if constexpr (IDF == 8)
+        tree_union_fast<NPL, IDF, EW, R>(status, sm, k, b, N, L, E, ids, union_count, union_total,
+                                         union_bits, expert_hist);
+    else
+        tree_union_generic<NPL, IDF, KT, EW, R / 2>(status, sm, k, b, N, L, K, E, idb, ids,
+                                                    union_count, union_total, union_bits, expert_hist);
 }
 
 }  // namespace evict

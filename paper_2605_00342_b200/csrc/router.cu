@@ -1,15 +1,415 @@
-// router.cu — A8: router logits on tcgen05 tensor cores + TopK + expert union.
+// router.cu — A8 → A7: router logits of the kept draft nodes on tcgen05 tensor
+// cores, TopK, and the per-layer expert union (Eq. 4–5).
+//
+// One CTA = (layer l, 128 packed verify rows).  D[128 rows][128 experts] =
+// H·W_gᵀ accumulates in TMEM (128 fp32 columns) over d in 64-wide k-blocks:
+//   warps 0–3  gather the rows' hidden states (cp.async, 16 B per thread,
+//              128-byte XOR swizzle) into a 6-stage ring, then run the
+//              epilogue: tcgen05.ld → per-row TopK (logit desc, expert asc)
+//              → warp-aggregated atomicOr into the tree's union bitset
+//   warp 4     one elected thread issues tcgen05.mma (M128 N128 K16, bf16 →
+//              fp32, both operands K-major SWIZZLE_128B) and tcgen05.commit
+//   warp 5     one thread streams W_g k-blocks with TMA (cp.async.bulk.tensor)
+// mbarriers: full[s] (128 producer arrivals + TMA tx bytes), empty[s]
+// (tcgen05.commit), tmem_full.  A finalize kernel turns bitsets into counts.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "evict.h"
+#include "evict_launch.h"
+
+namespace evict {
+namespace router {
+
+constexpr int BM = 128, BN = 128, BK = 64;
+constexpr int STAGES = 6;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_BYTES = BN * BK * 2;  // 16 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int THREADS = 192;
+constexpr int NPROD = 128;
+constexpr int KMAX = 16;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, ridx*/ + 512;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(bar),
+        "r"(phase)
+        : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int x, int y)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr)
+{
+    return (uint64_t)((addr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+// Instruction descriptor: kind::f16, A/B bf16, D fp32, K-major, M=128, N=128.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate)
+{
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32])
+{
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+
+struct Params {
+    const uint16_t *hidden;        // bf16 [L][BNrows][d]
+    const int32_t *verify_offsets; // [B+1]
+    const int32_t *retrieve_index; // [cap]
+    int L, B, N, d, K;
+    unsigned long long *bits;      // [B][L][2]
+    int32_t *topk_ids;             // [L][B*N][K] or null
+    float *dbg_logits;             // [L][B*N][128] or null (debug entry point only)
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+k_router(const __grid_constant__ CUtensorMap wmap, Params p)
+{
+    extern __shared__ uint8_t smem_raw[];
+    const int T = __ldg(p.verify_offsets + p.B);
+    const int m0 = blockIdx.x * BM;
+    if (m0 >= T) return;                      // uniform per CTA, before any barrier
+    const int l = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t *base = smem_raw + (base_u32 - smem_u32(smem_raw));
+    uint8_t *meta = base + STAGES * STAGE_BYTES;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(meta);   // full[S], empty[S], tmem_full
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(meta + 8 * (2 * STAGES + 1));
+    int *ridx = reinterpret_cast<int *>(meta + 256);
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + STAGES), tfull = smem_u32(bars + 2 * STAGES);
+    auto A = [&](int s) { return base_u32 + s * STAGE_BYTES; };
+    auto Bs = [&](int s) { return base_u32 + s * STAGE_BYTES + A_BYTES; };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(full0 + 8 * s, NPROD + 1);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        mbar_init(tfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 4) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x < BM) {
+        const int r = m0 + threadIdx.x;
+        ridx[threadIdx.x] = r < T ? __ldg(p.retrieve_index + r) : -1;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+    const int KB = p.d / BK;
+    const size_t BNrows = (size_t)p.B * p.N;
+
+    if (warp < 4) {
+        // ---- producers: gather 128 rows × 64 bf16 per stage, swizzled
+        const int t = threadIdx.x, c = t & 7, r0 = t >> 3;
+        const uint16_t *hl = p.hidden + (size_t)l * BNrows * p.d;
+        for (int kb = 0; kb < KB; kb++) {
+            const int s = kb % STAGES;
+            if (kb >= STAGES) mbar_wait(empty0 + 8 * s, ((kb / STAGES) - 1) & 1);
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int row = r0 + 16 * j;
+                const int rid = ridx[row];
+                const uint16_t *src = hl + (size_t)(rid < 0 ? 0 : rid) * p.d + kb * BK + c * 8;
+                cp_async16(A(s) + row * 128 + ((c ^ (row & 7)) << 4), src, rid < 0 ? 0u : 16u);
+            }
+            cp_async_commit();
+            if (kb >= STAGES - 1) {
+                cp_async_wait<STAGES - 1>();
+                fence_proxy_async();
+                mbar_arrive(full0 + 8 * ((kb - (STAGES - 1)) % STAGES));
+            }
+        }
+        cp_async_wait<0>();
+        fence_proxy_async();
+        for (int kb = (KB > STAGES - 1 ? KB - (STAGES - 1) : 0); kb < KB; kb++) mbar_arrive(full0 + 8 * (kb % STAGES));
+
+        // ---- epilogue: TMEM → registers → TopK → union bits
+        mbar_wait(tfull, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int row = warp * 32 + lane;
+        const int r = m0 + row;
+        const bool valid = r < T;
+        float bv[KMAX];
+        int bi[KMAX];
+#pragma unroll
+        for (int j = 0; j < KMAX; j++) { bv[j] = -__int_as_float(0x7f800000); bi[j] = 0x7fffffff; }
+        float thr = bv[0];
+        const int K = p.K;
+#pragma unroll 1
+        for (int chunk = 0; chunk < BN / 32; chunk++) {
+            float v[32];
+            tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + chunk * 32, v);
+            if (p.dbg_logits && valid)
+                for (int i = 0; i < 32; i++) p.dbg_logits[((size_t)l * BNrows + r) * BN + chunk * 32 + i] = v[i];
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+                if (v[i] > thr) {                 // later experts never beat equal logits
+                    float cv = v[i];
+                    int ci = chunk * 32 + i;
+#pragma unroll
+                    for (int j = 0; j < KMAX; j++) {
+                        if (j < K) {
+                            // full key (logit desc, expert asc): a displaced entry
+                            // keeps its place ahead of an equal logit with a larger id
+                            const bool sw = cv > bv[j] || (cv == bv[j] && ci < bi[j]);
+                            const float tv = bv[j];
+                            const int ti = bi[j];
+                            bv[j] = sw ? cv : tv;
+                            bi[j] = sw ? ci : ti;
+                            cv = sw ? tv : cv;
+                            ci = sw ? ti : ci;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < KMAX; j++)
+                        if (j == K - 1) thr = bv[j];
+                }
+            }
+        }
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int j = 0; j < KMAX; j++)
+            if (j < K && bi[j] < BN) w[bi[j] >> 5] |= 1u << (bi[j] & 31);
+        if (valid && p.topk_ids) {
+#pragma unroll
+            for (int j = 0; j < KMAX; j++)
+                if (j < K) p.topk_ids[((size_t)l * BNrows + r) * K + j] = bi[j];
+        }
+        const int tree = valid ? ridx[row] / p.N : -1;
+        unsigned pending = __ballot_sync(0xffffffffu, valid);
+        while (pending) {
+            const int leader = __ffs(pending) - 1;
+            const int tb = __shfl_sync(0xffffffffu, tree, leader);
+            const unsigned grp = __ballot_sync(0xffffffffu, valid && tree == tb);
+            const bool in = (grp >> lane) & 1u;
+            uint32_t o[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) o[q] = __reduce_or_sync(0xffffffffu, in ? w[q] : 0u);
+            if (lane == leader) {
+                unsigned long long *dst = p.bits + ((size_t)tb * p.L + l) * 2;
+                atomicOr(dst, (unsigned long long)o[0] | ((unsigned long long)o[1] << 32));
+                atomicOr(dst + 1, (unsigned long long)o[2] | ((unsigned long long)o[3] << 32));
+            }
+            pending &= ~grp;
+        }
+    } else if (warp == 4) {
+        // ---- MMA issuer
+        if (lane == 0) {
+            for (int kb = 0; kb < KB; kb++) {
+                const int s = kb % STAGES;
+                mbar_wait(full0 + 8 * s, (kb / STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int k = 0; k < BK / 16; k++)
+                    umma_bf16(tmem, umma_desc(A(s) + 32 * k), umma_desc(Bs(s) + 32 * k), (kb | k) != 0);
+                umma_commit(empty0 + 8 * s);
+            }
+            umma_commit(tfull);
+        }
+        __syncwarp();
+    } else {
+        // ---- W_g k-blocks via TMA
+        if (lane == 0) {
+            for (int kb = 0; kb < KB; kb++) {
+                const int s = kb % STAGES;
+                if (kb >= STAGES) mbar_wait(empty0 + 8 * s, ((kb / STAGES) - 1) & 1);
+                mbar_arrive_tx(full0 + 8 * s, B_BYTES);
+                tma_load_2d(Bs(s), &wmap, full0 + 8 * s, kb * BK, l * BN);
+            }
+        }
+        __syncwarp();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 4) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+    }
+}
+
+__global__ void k_finalize(int B, int L, const unsigned long long *bits, int32_t *count, int32_t *total)
+{
+    const int b = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (b >= B) return;
+    int tot = 0;
+    for (int l = lane; l < L; l += 32) {
+        const int c = __popcll(bits[((size_t)b * L + l) * 2]) + __popcll(bits[((size_t)b * L + l) * 2 + 1]);
+        count[(size_t)b * L + l] = c;
+        tot += c;
+    }
+    tot = __reduce_add_sync(0xffffffffu, tot);
+    if (total && lane == 0) total[b] = tot;
+}
+
+// ---------------------------------------------------------------- host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn()
+{
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    });
+    return fn;
+}
+
+}  // namespace router
+}  // namespace evict
+
+using namespace evict::router;
+
+static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *verify_offsets,
+                                  const int32_t *retrieve_index, const evict_router_t *rt,
+                                  int32_t *union_count, int32_t *union_total, uint64_t *union_bits,
+                                  int32_t *topk_ids, float *dbg_logits, void *stream);
 
 extern "C" evict_status_t evict_router_union(const evict_trees_t *trees, const int32_t *verify_offsets,
-                                             const int32_t *retrieve_index, const evict_router_t *router,
+                                             const int32_t *retrieve_index, const evict_router_t *rt,
                                              int32_t *union_count, int32_t *union_total,
                                              uint64_t *union_bits, int32_t *topk_ids, void *stream)
 {
-    (void)trees; (void)verify_offsets; (void)retrieve_index; (void)router; (void)union_count;
-    (void)union_total; (void)union_bits; (void)topk_ids; (void)stream;
-    return EVICT_ERR_UNSUPPORTED;
+    return router_impl(trees, verify_offsets, retrieve_index, rt, union_count, union_total, union_bits,
+                       topk_ids, nullptr, stream);
+}
+
+// Debug entry point (not part of include/evict.h): also dumps the raw fp32 logits.
+extern "C" evict_status_t evict_router_union_debug(const evict_trees_t *trees, const int32_t *verify_offsets,
+                                                   const int32_t *retrieve_index, const evict_router_t *rt,
+                                                   int32_t *union_count, int32_t *union_total,
+                                                   uint64_t *union_bits, int32_t *topk_ids, float *logits,
+                                                   void *stream)
+{
+    return router_impl(trees, verify_offsets, retrieve_index, rt, union_count, union_total, union_bits,
+                       topk_ids, logits, stream);
+}
+
+static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *verify_offsets,
+                                  const int32_t *retrieve_index, const evict_router_t *rt,
+                                  int32_t *union_count, int32_t *union_total, uint64_t *union_bits,
+                                  int32_t *topk_ids, float *dbg_logits, void *stream)
+{
+    if (!trees || !rt || !verify_offsets || !retrieve_index || !union_count || !union_bits)
+        return EVICT_ERR_INVALID_ARG;
+    if (trees->batch < 1 || trees->max_nodes < 1 || trees->max_nodes > EVICT_MAX_NODES) return EVICT_ERR_INVALID_ARG;
+    if (!rt->hidden || !rt->w_gate || rt->num_layers < 1 || rt->num_layers > EVICT_MAX_LAYERS)
+        return EVICT_ERR_INVALID_ARG;
+    if (rt->top_k < 1 || rt->top_k > EVICT_MAX_TOPK || rt->top_k > rt->num_experts) return EVICT_ERR_INVALID_ARG;
+    if (rt->hidden_dim < 64 || rt->hidden_dim % 64) return EVICT_ERR_INVALID_ARG;
+    if (((uintptr_t)rt->hidden | (uintptr_t)rt->w_gate) & 15) return EVICT_ERR_INVALID_ARG;
+    if (rt->num_experts != 128) return EVICT_ERR_UNSUPPORTED;
+    if (evict::dev_sms() <= 0) return EVICT_ERR_UNSUPPORTED;
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return EVICT_ERR_UNSUPPORTED;
+    const int L = rt->num_layers, E = rt->num_experts, d = rt->hidden_dim;
+    const int B = trees->batch, N = trees->max_nodes;
+    CUtensorMap map;
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)L * E};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 2};
+    cuuint32_t box[2] = {BK, BN};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(rt->w_gate), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return EVICT_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    static std::once_flag attr_once;
+    std::call_once(attr_once, [] { cudaFuncSetAttribute(k_router, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES); });
+    if (cudaMemsetAsync(union_bits, 0, sizeof(uint64_t) * (size_t)B * L * 2, s) != cudaSuccess) return EVICT_ERR_CUDA;
+    Params p;
+    p.hidden = (const uint16_t *)rt->hidden;
+    p.verify_offsets = verify_offsets;
+    p.retrieve_index = retrieve_index;
+    p.L = L; p.B = B; p.N = N; p.d = d; p.K = rt->top_k;
+    p.bits = reinterpret_cast<unsigned long long *>(union_bits);
+    p.topk_ids = topk_ids;
+    p.dbg_logits = dbg_logits;
+    dim3 grid((unsigned)(((size_t)B * N + BM - 1) / BM), (unsigned)L);
+    k_router<<<grid, THREADS, SMEM_BYTES, s>>>(map, p);
+    if (cudaGetLastError() != cudaSuccess) return EVICT_ERR_CUDA;
+    k_finalize<<<(B + 7) / 8, 256, 0, s>>>(B, L, reinterpret_cast<const unsigned long long *>(union_bits),
+                                           union_count, union_total);
+    return cudaGetLastError() == cudaSuccess ? EVICT_OK : EVICT_ERR_CUDA;
 }

@@ -1,0 +1,103 @@
+"""A8 router GEMM (tcgen05) + TopK + union vs the oracle and vs torch.matmul/topk (needs a B200)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from oracle.parity import compare_union
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ev():
+    import paper_2605_00342_b200 as ev
+    ev.lib()
+    return ev
+
+
+def cu(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def bf16(a_bits):
+    import torch
+    return cu(a_bits.view(np.int16)).view(torch.bfloat16)
+
+
+def kept_rows(ev, B, N, steps, topk, seed):
+    P, Q, n = gen.trees(seed, B, N, steps, topk)
+    cost = gen.cost_table(N)
+    sel = ev.evict_select(cu(P), cu(Q), cu(cost), n_nodes=cu(n))
+    b = ev.evict_build_verify_tree(cu(P), sel["keep_bits"], n_nodes=cu(n))
+    return P, n, sel, b
+
+
+@pytest.mark.parametrize("B,N,steps,topk,L,d,K", [
+    (1, 60, 6, 10, 48, 2048, 8),      # c2 shape
+    (16, 60, 6, 10, 6, 4096, 8),      # c3 shape, fewer layers
+    (64, 128, 8, 10, 4, 2048, 8),     # c4 shape, fewer layers
+    (5, 32, 4, 8, 3, 64, 2),          # small d, K=2
+    (3, 8, 3, 2, 2, 128, 16),         # K = 16
+])
+def test_router_integer_inputs_bit_exact(ev, B, N, steps, topk, L, d, K):
+    """Integer-valued bf16 h, W_g ⇒ every fp32 partial sum is exact ⇒ TopK (with the
+    (logit desc, expert asc) tie rule) must match the fp64 oracle bit for bit."""
+    E = 128
+    P, n, sel, b = kept_rows(ev, B, N, steps, topk, seed=21)
+    h = gen.hidden(31, B, N, L, d, mode=0)
+    w = gen.wgate(32, L, E, d, mode=0)
+    g = ev.evict_router_union(b["verify_offsets"], b["retrieve_index"], bf16(h), bf16(w), K, B, N,
+                              with_topk=True)
+    keep = sel["keep_bits"].cpu().numpy().view(np.uint64)
+    o = oracle.router_union(keep, h, w, K, threads=8)
+    gg = {k: v.cpu().numpy() for k, v in g.items()}
+    assert not compare_union(o, gg)
+    # per-row TopK ids, in rank order
+    T = int(b["verify_offsets"][-1])
+    ridx = b["retrieve_index"].cpu().numpy()
+    rows = np.random.default_rng(0).choice(T, min(T, 40), replace=False)
+    for l in range(L):
+        for r in rows:
+            ids, _, _ = oracle.router_topk(h[l, ridx[r]], w[l], K)
+            assert gg["topk_ids"][l, r].tolist() == ids.tolist(), (l, r)
+
+
+def test_router_vs_torch_normal_inputs(ev):
+    """bf16 N(0,1) inputs: compare with the library routine torch.matmul (fp32) + torch.topk,
+    excluding rows whose K-th/(K+1)-th logit gap is within fp32 accumulation error."""
+    import torch
+    B, N, L, d, K, E = 16, 60, 5, 2048, 8, 128
+    P, n, sel, b = kept_rows(ev, B, N, 6, 10, seed=5)
+    h = gen.hidden_cuda(41, B, N, L, d, mode=1)
+    w = gen.wgate_cuda(42, L, E, d, mode=1, scale_log2=-5)
+    g = ev.evict_router_union(b["verify_offsets"], b["retrieve_index"], h, w, K, B, N, with_topk=True)
+    T = int(b["verify_offsets"][-1])
+    ridx = b["retrieve_index"][:T].long()
+    checked = excluded = 0
+    for l in range(L):
+        x = h[l, ridx].float()
+        lg = x @ w[l].float().t()
+        srt = torch.sort(lg, dim=1, descending=True, stable=True)
+        gap = srt.values[:, K - 1] - srt.values[:, K]
+        tol = d * 2.0 ** -22 * (x.abs() @ w[l].float().abs().t()).max(dim=1).values
+        ok = gap > tol
+        ref = torch.sort(srt.indices[:, :K], dim=1).values
+        got = torch.sort(g["topk_ids"][l, :T].long(), dim=1).values
+        same = (ref == got).all(dim=1)
+        assert bool(same[ok].all()), (l, int((~same[ok]).sum()))
+        checked += int(ok.sum())
+        excluded += int((~ok).sum())
+    assert checked > 0.7 * (checked + excluded)
+
+
+def test_router_rejects_unsupported(ev):
+    import torch
+    h = torch.zeros((1, 8, 64), dtype=torch.bfloat16, device="cuda")
+    w = torch.zeros((1, 64, 64), dtype=torch.bfloat16, device="cuda")     # E = 64
+    off = torch.tensor([0, 1], dtype=torch.int32, device="cuda")
+    ri = torch.zeros(8, dtype=torch.int32, device="cuda")
+    with pytest.raises(ev.EvictError) as e:
+        ev.evict_router_union(off, ri, h, w, 2, 1, 8)
+    assert e.value.code == ev.EVICT_ERR_UNSUPPORTED
