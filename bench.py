@@ -265,6 +265,79 @@ def latency_b64(ev, torch, gen, N=60, steps=6, topk=10, seed=4, replays=2000):
     return out
 
 
+def time_fused(ev, torch, call, stream, reps):
+    """Mean device time of `call` (a FusedCall) over reps launches, CUDA events on `stream`."""
+    for _ in range(3):
+        call(stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps):
+        call(stream)
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def mask_variant(ev, gen, torch, P, Q, n, cost, ids8, M, stream, reps):
+    """Same trees with routing re-encoded as one-hot expert masks (16 B per node-layer):
+    the union becomes a pure OR stream."""
+    masks = gen.ids_to_mask_cuda(ids8, N_EXPERTS)
+    call = ev.FusedCall(P, Q, cost, masks, N_EXPERTS, n_nodes=n)
+    ms = time_fused(ev, torch, call, stream, reps)
+    k_sum = int(call.buffers.t["k_star"].sum())
+    n_sum = int(n.sum())
+    abytes, parts = algorithmic_bytes(n_sum, k_sum, M, 8, id_format="mask")
+    peak, _ = hbm_peak()
+    ach = abytes / (ms / 1e3) / 1e9
+    del call, masks
+    torch.cuda.empty_cache()
+    return {"id_format": "mask", "value": M / (ms / 1e3), "unit": "trees/s", "kernel_ms": ms,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "algorithmic_bytes_per_launch": abytes}}
+
+
+def router_bench(ev, gen, torch, stream):
+    """A8: router logits GEMM (tcgen05) + TopK + union on the C2/C3/C4 shapes.
+    Bytes = L·(T·d + E·d)·2, flops = 2·L·T·d·E with T = packed kept rows (Σ k*)."""
+    import numpy as np
+    res = {}
+    peaks_ = peaks()
+    tf_peak = float(peaks_.get("bf16_tflops", 1590.0))
+    hbm, _ = hbm_peak()
+    for name, B, Nn, steps, topk, L, d in (("c2", 1, 60, 6, 10, 48, 2048),
+                                            ("c3_b16", 16, 60, 6, 10, 94, 4096),
+                                            ("c4", 64, 128, 8, 10, 48, 2048)):
+        P, Q, n = gen.trees(3, B, Nn, steps, topk)
+        cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+        sel = ev.evict_select(cu(P), cu(Q), cu(gen.cost_table(Nn)), n_nodes=cu(n))
+        b = ev.evict_build_verify_tree(cu(P), sel["keep_bits"], n_nodes=cu(n))
+        h = gen.hidden_cuda(11, B, Nn, L, d, mode=1)
+        w = gen.wgate_cuda(12, L, N_EXPERTS, d, mode=1, scale_log2=-5)
+        T = int(b["verify_offsets"][-1])
+        rc = ev.RouterCall(b["verify_offsets"], b["retrieve_index"], h, w, TOP_K, B, Nn)
+        for _ in range(3):
+            rc(stream)
+        reps = 50
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            rc(stream)
+        e1.record(stream)
+        e1.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / reps
+        byt = L * (T * d + N_EXPERTS * d) * 2
+        fl = 2.0 * L * T * d * N_EXPERTS
+        res[name] = {"B": B, "N": Nn, "L": L, "d": d, "rows": T, "us": us,
+                     "gbs": byt / (us / 1e6) / 1e9, "hbm_frac": byt / (us / 1e6) / 1e9 / hbm,
+                     "tflops": fl / (us / 1e6) / 1e12, "tensor_frac": fl / (us / 1e6) / 1e12 / tf_peak,
+                     "bound": "hbm (intensity <= E = 128 flop/B < ridge)"}
+        del h, w
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_native(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -381,7 +454,17 @@ def run_native(args, rank, world, local_rank):
     }
     # ---- end-to-end through the public API with host buffers (rank-local)
     result["e2e"] = e2e(args, ev, torch, P, Q, n, cost, ids, M, world, stream)
+    if not args.no_extras and args.id_format == "u8":
+        try:
+            result["variants"] = {"mask": mask_variant(ev, gen, torch, P, Q, n, cost, ids, M, stream,
+                                                       max(3, K // 2))}
+        except Exception as e:  # pragma: no cover
+            result["variants"] = {"mask": {"error": repr(e)}}
     if rank == 0 and not args.no_extras:
+        try:
+            result["router"] = router_bench(ev, gen, torch, stream)
+        except Exception as e:  # pragma: no cover
+            result["router"] = {"error": repr(e)}
         try:
             result["latency"] = latency_b64(ev, torch, gen)
             result["latency"].update({k.replace("n60", "n128"): v for k, v in

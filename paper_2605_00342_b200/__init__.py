@@ -313,6 +313,35 @@ def evict_router_union(verify_offsets, retrieve_index, hidden, w_gate, top_k, ba
     return out
 
 
+class RouterCall:
+    """A pre-marshalled evict_router_union call with pre-allocated outputs (timing loops, graphs)."""
+
+    def __init__(self, verify_offsets, retrieve_index, hidden, w_gate, top_k, batch, max_nodes,
+                 with_topk=False):
+        L, BN, d = hidden.shape
+        E = w_gate.shape[1]
+        dev = hidden.device
+        EW = (E + 63) // 64
+        self.keep = (verify_offsets, retrieve_index, hidden, w_gate)
+        self.t = dict(union_count=torch.empty((batch, L), dtype=torch.int32, device=dev),
+                      union_total=torch.empty(batch, dtype=torch.int32, device=dev),
+                      union_bits=torch.empty((batch, L, EW), dtype=torch.int64, device=dev))
+        if with_topk:
+            self.t["topk_ids"] = torch.full((L, BN, top_k), -1, dtype=torch.int32, device=dev)
+        self.tr = _Trees(batch, max_nodes, None, None, None)
+        self.rt = _Router(L, E, top_k, d, _p(hidden), _p(w_gate))
+        self.args = (_p(verify_offsets), _p(retrieve_index))
+        self.fn = lib().evict_router_union
+
+    def __call__(self, stream=None):
+        rc = self.fn(ctypes.byref(self.tr), self.args[0], self.args[1], ctypes.byref(self.rt),
+                     _p(self.t["union_count"]), _p(self.t["union_total"]), _p(self.t["union_bits"]),
+                     _p(self.t.get("topk_ids")), _stream(stream))
+        if rc:
+            raise EvictError(rc, "evict_router_union")
+        return self.t
+
+
 # ----------------------------------------------------------------- stats (A9)
 def evict_batch_stats(k_star, e_hat, utility, union_count, status, max_nodes, n_nodes=None,
                       stream=None):

@@ -1,0 +1,430 @@
+// evict_group.cuh — sub-warp-per-tree select (A1–A5) and verify-tree build (A6).
+//
+// A group of G lanes owns one tree (G = 8 for N ≤ 64, G = 16 for N ≤ 128), so a
+// warp works on 32/G trees at once; lane g of a group owns the 8 consecutive
+// nodes 8g .. 8g+7 (two 16-byte vector loads per array).  Compared with one
+// warp per tree this cuts the per-tree instruction count several-fold: most
+// bitonic stages become register compare-exchanges inside a lane, the scan is
+// 8 serial adds + log2(G) shuffles, and every warp instruction serves 4 (or 2)
+// trees.  All shuffles stay inside the group (xor offsets < G, width G).
+//   A1 g_load            PAPER.md:48; readings Z4/Z9/Z10
+//   A2 g_levels          Eq. 7: synchronous sweeps, exact
+//                        serial root→leaf fp32 products
+//   A3–A5 g_rank_argmax  §3.2.1, Eq. 8–10
+//   A6 g_emit            Fig. 4(c), layout Z12
+#pragma once
+
+#include "evict_tree.cuh"
+
+namespace evict {
+namespace grp {
+
+constexpr int NP = 8;  // nodes per lane
+
+template <int G>
+struct GShape {
+    static constexpr int NMAX = G * NP;   // 64 or 128
+    static constexpr int W = NMAX / 64;   // 64-bit mask words
+    static constexpr int TPW = 32 / G;    // trees per warp
+};
+
+template <int G>
+__device__ __forceinline__ int gl() { return threadIdx.x & (G - 1); }
+template <int G>
+__device__ __forceinline__ int gidx() { return (threadIdx.x & 31) / G; }
+
+template <int G>
+__device__ __forceinline__ uint32_t g_or(uint32_t v)
+{
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v |= __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+template <int G>
+__device__ __forceinline__ uint32_t g_max(uint32_t v)
+{
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+        const uint32_t w = __shfl_xor_sync(kFull, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+template <int G>
+__device__ __forceinline__ int g_maxi(int v)
+{
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+        const int w = __shfl_xor_sync(kFull, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+template <int G>
+__device__ __forceinline__ uint64_t g_or64(uint64_t v)
+{
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v |= shfl_xor64(v, o);
+    return v;
+}
+
+template <int W>
+__device__ __forceinline__ int popc_below_w(const uint64_t (&m)[W], int i)
+{
+    int c = 0;
+#pragma unroll
+    for (int w = 0; w < W; w++) {
+        const int lo = w * 64;
+        const uint64_t mk = i >= lo + 64 ? ~0ull : (i <= lo ? 0ull : ((1ull << (i - lo)) - 1ull));
+        c += __popcll(m[w] & mk);
+    }
+    return c;
+}
+template <int W>
+__device__ __forceinline__ bool bit_w(const uint64_t (&m)[W], int i)
+{
+    bool r = false;
+#pragma unroll
+    for (int w = 0; w < W; w++)
+        if ((i >> 6) == w) r = (m[w] >> (i & 63)) & 1ull;
+    return r;
+}
+
+template <int G>
+struct GTree {
+    static constexpr int W = GShape<G>::W;
+    int par[NP];
+    float q[NP];
+    float sc[NP];
+    int dep[NP];
+    int n;
+    uint32_t status;  // EVICT_TREE_* ; inactive groups carry BAD_SIZE
+    int kstar;
+    float ehat, util;
+    uint64_t keep[W];  // identical in every lane of the group
+};
+
+// ------------------------------------------------------------ A1
+template <int G>
+__device__ __forceinline__ void g_load(GTree<G> &t, const int32_t *__restrict__ parent,
+                                       const float *__restrict__ q, const int32_t *__restrict__ n_nodes,
+                                       int b, int N, bool active)
+{
+    const int base = gl<G>() * NP;
+    const size_t row = (size_t)b * N;
+    int4 p0 = make_int4(-1, -1, -1, -1), p1 = p0;
+    float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
+    if (active && base < N) {
+        p0 = __ldg(reinterpret_cast<const int4 *>(parent + row + base));
+        q0 = __ldg(reinterpret_cast<const float4 *>(q + row + base));
+        if (base + NP <= N) {   // N % 4 == 0: the second half is all in or all out
+            p1 = __ldg(reinterpret_cast<const int4 *>(parent + row + base + 4));
+            q1 = __ldg(reinterpret_cast<const float4 *>(q + row + base + 4));
+        }
+    }
+    t.par[0] = p0.x; t.par[1] = p0.y; t.par[2] = p0.z; t.par[3] = p0.w;
+    t.par[4] = p1.x; t.par[5] = p1.y; t.par[6] = p1.z; t.par[7] = p1.w;
+    t.q[0] = q0.x; t.q[1] = q0.y; t.q[2] = q0.z; t.q[3] = q0.w;
+    t.q[4] = q1.x; t.q[5] = q1.y; t.q[6] = q1.z; t.q[7] = q1.w;
+    t.n = active ? (n_nodes ? __ldg(n_nodes + b) : N) : 0;
+    uint32_t st = (t.n < 1 || t.n > N) ? EVICT_TREE_BAD_SIZE : 0u;
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        const int i = base + r;
+        if (i < t.n) {
+            if (i == 0) {
+                if (t.par[r] != -1) st |= EVICT_TREE_BAD_PARENT;
+            } else {
+                if (t.par[r] < 0 || t.par[r] >= i) st |= EVICT_TREE_BAD_PARENT;
+                const float qq = t.q[r];
+                if (!(qq >= 0.f && qq <= 1.f)) st |= EVICT_TREE_BAD_PROB;
+            }
+        }
+        if (t.q[r] == 0.f) t.q[r] = 0.f;  // canonicalise -0.0 (Z9)
+    }
+    st = g_or<G>(st);
+    t.status = (st & EVICT_TREE_BAD_SIZE) ? EVICT_TREE_BAD_SIZE : st;
+}
+
+template <int G>
+__device__ __forceinline__ void g_load_cost(float (&c)[NP], GTree<G> &t, const float *__restrict__ cost)
+{
+    const int base = gl<G>() * NP;
+    uint32_t st = 0;
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        const int i = base + r;
+        c[r] = 1.f;
+        if (i < t.n && !(t.status & EVICT_TREE_BAD_SIZE)) {
+            c[r] = __ldg(cost + i);
+            if (!(c[r] > 0.f)) st |= EVICT_TREE_BAD_COST;
+            if (i == 0 && c[r] == __int_as_float(0x7f800000)) st |= EVICT_TREE_BAD_COST;
+        }
+    }
+    t.status |= g_or<G>(st);
+}
+
+// ------------------------------------------------------------ A2
+// sd: this group's (score bits, depth) array of NMAX entries in shared memory.
+template <int G, bool SCORES>
+__device__ __forceinline__ void g_levels(GTree<G> &t, int2 *sd)
+{
+    const int base = gl<G>() * NP;
+    bool live[NP];
+    int pidx[NP];
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        const int i = base + r;
+        live[r] = (t.status == 0) && (i > 0) && (i < t.n);
+        pidx[r] = live[r] ? t.par[r] : 0;
+        t.sc[r] = 1.f;
+        t.dep[r] = 0;
+        sd[i] = make_int2(__float_as_int(1.f), 0);
+    }
+    __syncwarp();
+    while (true) {
+        bool changed = false;
+        float ns[NP];
+        int nd[NP];
+#pragma unroll
+        for (int r = 0; r < NP; r++) {
+            const int2 pv = sd[pidx[r]];
+            float sv = t.sc[r];
+            if constexpr (SCORES) sv = __fmul_rn(__int_as_float(pv.x), t.q[r]);  // both ≥ +0
+            ns[r] = live[r] ? sv : t.sc[r];
+            nd[r] = live[r] ? pv.y + 1 : t.dep[r];
+            changed |= (__float_as_int(ns[r]) != __float_as_int(t.sc[r])) | (nd[r] != t.dep[r]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < NP; r++) {
+            t.sc[r] = ns[r];
+            t.dep[r] = nd[r];
+        }
+#pragma unroll
+        for (int r = 0; r < NP; r += 2)
+            *reinterpret_cast<int4 *>(&sd[base + r]) =
+                make_int4(__float_as_int(ns[r]), nd[r], __float_as_int(ns[r + 1]), nd[r + 1]);
+        __syncwarp();
+        if (!__any_sync(kFull, changed)) break;
+    }
+}
+
+// ------------------------------------------------------------ A3–A5
+// rk: this group's node → rank bytes (NMAX).  Writes order/prefix rows when
+// given (row of N entries), fills t.kstar/ehat/util/keep.
+template <int G>
+__device__ __forceinline__ void g_rank_argmax(GTree<G> &t, uint8_t *rk, const float (&c)[NP], int N,
+                                              int32_t *__restrict__ order_row,
+                                              float *__restrict__ prefix_row)
+{
+    constexpr int NMAX = GShape<G>::NMAX;
+    constexpr int W = GShape<G>::W;
+    const int g = gl<G>();
+    const int base = g * NP;
+    const bool ok = t.status == 0;
+    uint64_t key[NP];
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        const int i = base + r;
+        key[r] = (ok && i < t.n) ? (((uint64_t)(~__float_as_uint(t.sc[r])) << 32) | (uint32_t)i) : ~0ull;
+    }
+    // bitonic sort ascending on key == (score desc, index asc); element x = 8g + r
+#pragma unroll
+    for (int k = 2; k <= NMAX; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < NP) {
+#pragma unroll
+                for (int r = 0; r < NP; r++) {
+                    const int rp = r ^ j;
+                    if (rp > r) {
+                        const bool asc = (((base + r) & k) == 0);
+                        const uint64_t a = key[r], bb = key[rp];
+                        const bool sw = asc ? (a > bb) : (a < bb);
+                        key[r] = sw ? bb : a;
+                        key[rp] = sw ? a : bb;
+                    }
+                }
+            } else {
+                const int lj = j / NP;
+#pragma unroll
+                for (int r = 0; r < NP; r++) {
+                    const int x = base + r;
+                    const uint64_t o = shfl_xor64(key[r], lj);
+                    const bool take_min = (((x & j) == 0) == ((x & k) == 0));
+                    key[r] = take_min ? (o < key[r] ? o : key[r]) : (o > key[r] ? o : key[r]);
+                }
+            }
+        }
+    }
+    float sp[NP];
+    int node[NP];
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        node[r] = (int)(uint32_t)key[r];
+        sp[r] = __uint_as_float(~(uint32_t)(key[r] >> 32));
+        if (ok && base + r < t.n) rk[node[r]] = (uint8_t)(base + r);
+    }
+    // A4: S[k] = Σ_{j<k} Score(order[j])
+    float loc[NP];
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        acc = __fadd_rn(acc, sp[r]);
+        loc[r] = acc;
+    }
+    float incl = acc;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+        const float v = __shfl_up_sync(kFull, incl, o, G);
+        if (g >= o) incl = __fadd_rn(incl, v);
+    }
+    float excl = __shfl_up_sync(kFull, incl, 1, G);
+    if (g == 0) excl = 0.f;
+    float S[NP];
+    uint32_t Rb[NP];
+    uint32_t best = 0;
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        S[r] = __fadd_rn(excl, loc[r]);
+        const bool v = ok && base + r < t.n;
+        const float R = v ? __fdiv_rn(S[r], c[r]) : 0.f;   // A5: IEEE division, +inf cost ⇒ 0
+        Rb[r] = v ? __float_as_uint(R) : 0u;
+        best = Rb[r] > best ? Rb[r] : best;
+    }
+    const uint32_t mx = g_max<G>(best);
+    int rfirst = NP;
+#pragma unroll
+    for (int r = NP - 1; r >= 0; r--)
+        if (ok && Rb[r] == mx && base + r < t.n) rfirst = r;
+    const unsigned has = __ballot_sync(kFull, rfirst < NP);
+    const unsigned gm = (G == 32) ? has : ((has >> (gidx<G>() * G)) & ((1u << G) - 1u));
+    const int wl = gm ? __ffs(gm) - 1 : 0;                 // smallest k wins ties (Z3)
+    const int src = (threadIdx.x & 31 & ~(G - 1)) + wl;
+    const int rf = __shfl_sync(kFull, rfirst, src);
+    float Sk = 0.f, Rk = 0.f;
+#pragma unroll
+    for (int r = 0; r < NP; r++)
+        if (r == rf) { Sk = S[r]; Rk = __uint_as_float(Rb[r]); }
+    Sk = __shfl_sync(kFull, Sk, src);
+    Rk = __shfl_sync(kFull, Rk, src);
+    if (ok) {
+        t.ehat = Sk;
+        t.util = Rk;
+        t.kstar = wl * NP + rf + 1;
+    } else {
+        t.ehat = 0.f;
+        t.util = 0.f;
+        t.kstar = 0;
+    }
+    if (order_row != nullptr && base < N) {
+#pragma unroll
+        for (int r = 0; r < NP; r++) {
+            if (base + r < N) {
+                const bool v = ok && base + r < t.n;
+                order_row[base + r] = v ? node[r] : -1;
+                prefix_row[base + r] = v ? S[r] : 0.f;
+            }
+        }
+    }
+    __syncwarp();
+    // keep = order[0 .. k*): node i kept ⇔ rank(i) < k*
+    uint64_t local[W];
+#pragma unroll
+    for (int w = 0; w < W; w++) local[w] = 0ull;
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        const int i = base + r;
+        if (ok && i < t.n && rk[i] < t.kstar) local[i >> 6] |= 1ull << (i & 63);
+    }
+#pragma unroll
+    for (int w = 0; w < W; w++) t.keep[w] = g_or64<G>(local[w]);
+}
+
+// ------------------------------------------------------------ A6
+// Only kept nodes do work: each lane walks the set bits of its 8-node kept
+// mask.  Pass 1 ORs every kept non-root node's slot bit into its parent's
+// child mask (shared atomics); pass 2 builds each kept node's ancestor-or-self
+// row by walking the parent chain in the shared-memory record (depth steps, no
+// level loop) and emits the packed row.  par/dep: the tree's shared record
+// arrays; child: this group's scratch (NMAX × W words).
+template <int G>
+__device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W], int n, bool emit,
+                                       int k, int b, int N, int off, int pos_off,
+                                       const int8_t *par, const uint8_t *dep, uint64_t *child,
+                                       int32_t *__restrict__ kept_index,
+                                       int32_t *__restrict__ retrieve_index,
+                                       int32_t *__restrict__ positions,
+                                       int32_t *__restrict__ next_token,
+                                       int32_t *__restrict__ next_sibling,
+                                       uint64_t *__restrict__ tree_mask)
+{
+    constexpr int W = GShape<G>::W;
+    const int g = gl<G>();
+    const int base = g * NP;
+    uint32_t km = 0;
+    if (emit) {
+#pragma unroll
+        for (int r = 0; r < NP; r++) {
+            const int i = base + r;
+            if (i < n && bit_w<W>(keep, i)) km |= 1u << r;
+        }
+        for (int s = g; s < k; s += G)
+#pragma unroll
+            for (int w = 0; w < W; w++) child[s * W + w] = 0ull;
+    }
+    __syncwarp();
+    for (uint32_t m = km; m; m &= m - 1) {
+        const int i = base + __ffs(m) - 1;
+        if (i > 0) {
+            const int s = popc_below_w<W>(keep, i);
+            const int ps = popc_below_w<W>(keep, par[i]);
+            atomicOr(reinterpret_cast<unsigned long long *>(&child[ps * W + (s >> 6)]), 1ull << (s & 63));
+        }
+    }
+    __syncwarp();
+    for (uint32_t m = km; m; m &= m - 1) {
+        const int i = base + __ffs(m) - 1;
+        const int s = popc_below_w<W>(keep, i);
+        uint64_t row[W];
+#pragma unroll
+        for (int w = 0; w < W; w++) row[w] = 0ull;
+        for (int a = i; a >= 0; a = par[a]) {             // ancestor-or-self chain
+            const int sa = popc_below_w<W>(keep, a);
+#pragma unroll
+            for (int w = 0; w < W; w++)
+                if ((sa >> 6) == w) row[w] |= 1ull << (sa & 63);
+        }
+        int nt = -1, ns = -1;
+#pragma unroll
+        for (int w = W - 1; w >= 0; w--) {
+            const uint64_t cm = child[s * W + w];
+            if (cm) nt = w * 64 + __ffsll((long long)cm) - 1;
+        }
+        if (i > 0) {
+            const int ps = popc_below_w<W>(keep, par[i]);
+#pragma unroll
+            for (int w = W - 1; w >= 0; w--) {
+                uint64_t cm = child[ps * W + w];
+                const int lo = w * 64;
+                const uint64_t above = (s + 1 <= lo) ? ~0ull : (s + 1 >= lo + 64 ? 0ull : (~0ull << (s + 1 - lo)));
+                cm &= above;
+                if (cm) ns = lo + __ffsll((long long)cm) - 1;
+            }
+        }
+        const int rowi = off + s;
+        if (kept_index) kept_index[rowi] = i;
+        if (retrieve_index) retrieve_index[rowi] = b * N + i;
+        if (positions) positions[rowi] = pos_off + dep[i];
+        if (next_token) next_token[rowi] = nt;
+        if (next_sibling) next_sibling[rowi] = ns;
+        if (tree_mask) {
+#pragma unroll
+            for (int w = 0; w < W; w++) tree_mask[(size_t)rowi * W + w] = row[w];
+        }
+    }
+}
+
+}  // namespace grp
+}  // namespace evict

@@ -18,6 +18,7 @@
 
 #include "evict.h"
 #include "evict_tree.cuh"
+#include "evict_group.cuh"
 
 namespace evict {
 
@@ -219,7 +220,7 @@ __device__ __forceinline__ void tree_fill_klist(const TreeState<NPL> &t, WarpSla
 }
 
 // Flag bytes per warp for the shared-memory union (IDF 1/4): L × Epad.
-__host__ __device__ inline int union_epad(int E) { return E <= 128 ? 128 : 256; }
+__host__ __device__ inline int union_epad_u(int E) { return E <= 128 ? 128 : 256; }
 
 template <int NPL, int IDF, int KT, int EW, int CL>
 __global__ void __launch_bounds__(kWarps * 32) k_union(evict_trees_t tr, const uint64_t *keep_bits,
@@ -231,11 +232,12 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(evict_trees_t tr, const u
     __shared__ WarpSlab<NPL> slab[kWarps];
     constexpr int W = Shape<NPL>::W;
     const int warp = threadIdx.x >> 5, lane = lane_id();
-    const int Epad = union_epad(rt.num_experts);
-    uint8_t *flags = dsm + (size_t)warp * rt.num_layers * Epad;
+    const int Epad = union_epad_u(rt.num_experts);
+    const int nrounds = (2 * rt.num_layers + 31) / 32;
+    uint8_t *flags = dsm + (size_t)warp * 16 * Epad * nrounds;
     if constexpr (IDF == 1 || IDF == 4) {
         uint4 *f4 = reinterpret_cast<uint4 *>(flags);
-        for (int i = lane; i < rt.num_layers * Epad / 16; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
+        for (int i = lane; i < Epad * nrounds; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncwarp();
     }
     const int b = blockIdx.x * kWarps + warp;
@@ -259,151 +261,178 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(evict_trees_t tr, const u
     for (int w = 0; w < W; w++) k += __popcll(t.keep[w]);
     if (!t.status) tree_fill_klist<NPL>(t, sm);
     uint32_t st = t.status;
-    tree_union<NPL, IDF, KT, EW, CL>(st, sm, k, b, N, rt.num_layers, rt.top_k, rt.num_experts,
+    tree_union<NPL, IDF, KT, EW, CL>(st, sm.klist, k, b, N, rt.num_layers, rt.top_k, rt.num_experts,
                                      rt.id_format, rt.ids, flags, Epad, union_count, union_total,
                                      union_bits, expert_hist);
     if (status && lane == 0) status[b] = st;
 }
 
 // ------------------------------------------------------------ fused
-// One CTA tile = 32 consecutive trees, 4 per warp (warp w owns trees w, w+8,
-// w+16, w+24 of the tile), processed in three phases:
-//   A  per tree: A1–A5 select (outputs written), A7 union (outputs written),
-//      and an emit record (parent, depth, keep) parked in shared memory;
-//   B  one barrier: warp 0 scans the 32 row counts, publishes the tile
-//      aggregate, looks back for the tile prefix and fetches the next ticket;
-//   C  per tree: A6 build from the record at the packed offset.
-// Two barriers per 32 trees; union-time variance averages over 4 trees/warp.
-constexpr int kTreesPerWarp = 4;
-constexpr int kTile = kWarps * kTreesPerWarp;
+// One CTA tile = 32 consecutive trees.  A1–A5 and A6 run sub-warp-per-tree
+// (evict_group.cuh: G lanes per tree, 32/G trees per warp instruction); A7 runs
+// one warp per tree.  Phases per tile:
+//   A1  select every tree of the tile (outputs written) and park an emit record
+//       (parent, depth, keep) in shared memory;
+//   --  barrier; warp 0 scans the 32 row counts and publishes the tile aggregate
+//       (decoupled look-back state);
+//   A2  expert union, one warp per tree, 4 trees per warp;
+//   --  warp 0 looks back for the tile prefix (its wait overlapped A2) and
+//       takes the next tile ticket; barrier;
+//   C   verify-tree emit (A6) at the packed offsets.
+constexpr int kTile = 32;
 
-template <int NPL>
+template <int G>
 struct EmitRec {
-    static constexpr int NMAX = Shape<NPL>::NMAX;
-    static constexpr int W = Shape<NPL>::W;
+    static constexpr int NMAX = grp::GShape<G>::NMAX;
+    static constexpr int W = grp::GShape<G>::W;
     uint64_t keep[W];
-    int8_t par[NMAX];
-    uint8_t dep[NMAX];
+    alignas(8) int8_t par[NMAX];
+    alignas(8) uint8_t dep[NMAX];
     int n, k;
     uint32_t status;
 };
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
-template <int NPL>
-__host__ __device__ constexpr size_t fused_rec_offset() { return align16(sizeof(WarpSlab<NPL>) * kWarps); }
-template <int NPL>
-__host__ __device__ constexpr size_t fused_flags_offset()
+
+// Per-warp scratch: union flags (A2), or sweep state (A1), or emit rows/child (C).
+template <int G>
+__host__ __device__ constexpr size_t fused_scratch_fixed()
 {
-    return align16(fused_rec_offset<NPL>() + sizeof(EmitRec<NPL>) * kTile);
+    return align16(grp::GShape<G>::TPW * grp::GShape<G>::NMAX *
+                   (sizeof(int2) > 2 * 8 * grp::GShape<G>::W ? sizeof(int2) : 2 * 8 * grp::GShape<G>::W));
+}
+__host__ __device__ inline int union_epad(int E) { return E <= 128 ? 128 : 256; }
+template <int G>
+__host__ __device__ inline size_t fused_scratch_bytes(int L, int E, bool flags)
+{
+    const size_t f = flags ? (size_t)16 * union_epad(E) * ((2 * L + 31) / 32) : 0;   // R rounds of 16 layers
+    const size_t x = fused_scratch_fixed<G>();
+    return align16(f > x ? f : x);
+}
+template <int G>
+__host__ __device__ inline size_t fused_smem_bytes(int L, int E, bool flags)
+{
+    return (size_t)kWarps * fused_scratch_bytes<G>(L, E, flags)          // scratch
+           + align16(sizeof(EmitRec<G>) * kTile)                         // records
+           + (size_t)kWarps * grp::GShape<G>::TPW * grp::GShape<G>::NMAX  // ranks
+           + (size_t)kWarps * 128;                                       // klist
 }
 
 template <int NPL, int IDF, int KT, int EW, int CL>
-__global__ void __launch_bounds__(kWarps * 32, 2) k_fused(evict_trees_t tr, const float *cost,
+__global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, const float *cost,
                                                        int cost_stride, evict_routing_t rt,
                                                        evict_fused_out_t out, uint64_t *ws,
                                                        int ntiles)
 {
+    constexpr int G = NPL == 2 ? 8 : 16;
+    constexpr int TPW = grp::GShape<G>::TPW;
+    constexpr int NMAX = grp::GShape<G>::NMAX;
+    constexpr int W = grp::GShape<G>::W;
+    constexpr int PASSES = kTile / (kWarps * TPW);   // 1 (G=8) or 2 (G=16)
+    constexpr bool FLAGS = IDF == 1 || IDF == 4;
     extern __shared__ __align__(16) uint8_t dsm[];
-    // dynamic shared memory: [warp slabs][emit records][union flags]
-    WarpSlab<NPL> *slab = reinterpret_cast<WarpSlab<NPL> *>(dsm);
-    EmitRec<NPL> *rec = reinterpret_cast<EmitRec<NPL> *>(dsm + fused_rec_offset<NPL>());
     __shared__ int s_cnt[kTile], s_off[kTile], s_tile;
-    constexpr int W = Shape<NPL>::W;
     const int warp = threadIdx.x >> 5, lane = lane_id();
+    const int gi = grp::gidx<G>(), g = grp::gl<G>();
     const int N = tr.max_nodes;
     const int WN = (N + 63) / 64;
-    const int base = lane * NPL;
+    const int L = rt.num_layers, E = rt.num_experts;
+    const bool do_union = out.union_count != nullptr;
+    const size_t scratch = fused_scratch_bytes<G>(L, E, FLAGS && do_union);
+    uint8_t *wscr = dsm + (size_t)warp * scratch;
+    EmitRec<G> *rec = reinterpret_cast<EmitRec<G> *>(dsm + (size_t)kWarps * scratch);
+    uint8_t *ranks = reinterpret_cast<uint8_t *>(rec) + align16(sizeof(EmitRec<G>) * kTile);
+    uint8_t *rk = ranks + ((size_t)warp * TPW + gi) * NMAX;
+    uint8_t *klist = ranks + (size_t)kWarps * TPW * NMAX + warp * 128;
+    const int Epad = union_epad(E);
     unsigned *ticket = reinterpret_cast<unsigned *>(ws);
     uint64_t *states = ws + 1;
-    WarpSlab<NPL> &sm = slab[warp];
-    const int Epad = union_epad(rt.num_experts);
-    uint8_t *flags = dsm + fused_flags_offset<NPL>() + (size_t)warp * rt.num_layers * Epad;
-    if constexpr (IDF == 1 || IDF == 4) {
-        if (out.union_count) {
-            uint4 *f4 = reinterpret_cast<uint4 *>(flags);
-            for (int i = lane; i < rt.num_layers * Epad / 16; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
-            __syncwarp();
-        }
-    }
     if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
     __syncthreads();
     int tile = s_tile;
     while (tile < ntiles) {
-        // ---------------- phase A1: select per tree (+ emit record)
+        // ---------------- A1: select, sub-warp per tree
 #pragma unroll 1
-        for (int it = 0; it < kTreesPerWarp; it++) {
-            const int slot = warp + kWarps * it;
+        for (int pass = 0; pass < PASSES; pass++) {
+            const int slot = pass * (kWarps * TPW) + warp * TPW + gi;
             const int b = tile * kTile + slot;
-            int k = 0;
-            if (b < tr.batch) {
-                TreeState<NPL> t;
-                tree_load_validate<NPL>(t, tr, tr.parent, tr.q, tr.n_nodes, b, N);
-                float c[NPL];
-                if (!(t.status & EVICT_TREE_BAD_SIZE)) tree_load_cost<NPL>(c, t, cost + (size_t)b * cost_stride);
-                int32_t *orow = out.order ? out.order + (size_t)b * N : nullptr;
-                float *prow = out.prefix_sums ? out.prefix_sums + (size_t)b * N : nullptr;
-                if (!t.status) {
-                    tree_levels<NPL, true>(t, sm);
-                    tree_rank_argmax<NPL>(t, sm, c, N, orow, prow);
-                    k = t.kstar;
-                } else {
-                    t.kstar = 0; t.ehat = 0.f; t.util = 0.f;
-#pragma unroll
-                    for (int w = 0; w < W; w++) t.keep[w] = 0ull;
-                    if (orow)
-                        for (int p = lane; p < N; p += 32) { orow[p] = -1; prow[p] = 0.f; }
-                }
-                if (lane == 0) {
+            const bool active = b < tr.batch;
+            grp::GTree<G> t;
+            grp::g_load<G>(t, tr.parent, tr.q, tr.n_nodes, b, N, active);
+            float c[grp::NP];
+            grp::g_load_cost<G>(c, t, cost + (size_t)(active ? b : 0) * cost_stride);
+            int2 *sd = reinterpret_cast<int2 *>(wscr) + gi * NMAX;
+            grp::g_levels<G, true>(t, sd);
+            int32_t *orow = (active && out.order) ? out.order + (size_t)b * N : nullptr;
+            float *prow = (active && out.prefix_sums) ? out.prefix_sums + (size_t)b * N : nullptr;
+            grp::g_rank_argmax<G>(t, rk, c, N, orow, prow);
+            const int k = t.kstar;
+            if (active) {
+                if (g == 0) {
                     if (out.k_star) out.k_star[b] = t.kstar;
                     if (out.e_hat) out.e_hat[b] = t.ehat;
                     if (out.utility) out.utility[b] = t.util;
+                    s_cnt[slot] = k;
                 }
-                if (out.keep_bits && lane < WN) out.keep_bits[(size_t)b * WN + lane] = t.keep[lane < W ? lane : 0];
-                EmitRec<NPL> &er = rec[slot];
+                if (out.keep_bits && g < WN) out.keep_bits[(size_t)b * WN + g] = t.keep[g < W ? g : 0];
+                EmitRec<G> &er = rec[slot];
+                const int base = g * grp::NP;
+                uint32_t pw[2] = {0u, 0u}, dw[2] = {0u, 0u};
 #pragma unroll
-                for (int r = 0; r < NPL; r++) {
-                    er.par[base + r] = (int8_t)t.par[r];
-                    er.dep[base + r] = (uint8_t)t.dep[r];
+                for (int r = 0; r < grp::NP; r++) {
+                    pw[r >> 2] |= (uint32_t)(t.par[r] & 0xff) << (8 * (r & 3));
+                    dw[r >> 2] |= (uint32_t)(t.dep[r] & 0xff) << (8 * (r & 3));
                 }
-                if (lane < W) er.keep[lane] = t.keep[lane];
-                if (lane == 0) { er.n = t.n; er.k = k; er.status = t.status; }
+                *reinterpret_cast<uint2 *>(&er.par[base]) = make_uint2(pw[0], pw[1]);
+                *reinterpret_cast<uint2 *>(&er.dep[base]) = make_uint2(dw[0], dw[1]);
+                if (g < W) er.keep[g] = t.keep[g];
+                if (g == 0) { er.n = t.n; er.k = k; er.status = t.status; }
+            } else if (g == 0) {
+                s_cnt[slot] = 0;
             }
-            if (lane == 0) s_cnt[slot] = k;
+            __syncwarp();
         }
-        // ---------------- tile aggregate published as soon as every tree is selected
+        // ---------------- tile aggregate
         __syncthreads();
         int incl = 0;
         if (warp == 0) {
-            const int c = s_cnt[lane];             // kTile == 32 == warp size
-            incl = c;
+            const int cc = s_cnt[lane];
+            incl = cc;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                int v = __shfl_up_sync(kFull, incl, o);
+                const int v = __shfl_up_sync(kFull, incl, o);
                 if (lane >= o) incl += v;
             }
-            s_off[lane] = incl - c;
+            s_off[lane] = incl - cc;
             if (lane == 31) st_release(states + tile, (tile == 0 ? kInc : kAgg) | (uint64_t)incl);
         }
-        // ---------------- phase A2: expert union per tree (the look-back latency hides here)
-        if (out.union_count) {
+        // ---------------- A2: expert union, one warp per tree
+        if (do_union) {
+            if constexpr (FLAGS) {
+                uint4 *f4 = reinterpret_cast<uint4 *>(wscr);
+                const int nz = Epad * ((2 * L + 31) / 32);   // uint4 words: R rounds × Epad·16 B
+                for (int i = lane; i < nz; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
+                __syncwarp();
+            }
 #pragma unroll 1
-            for (int it = 0; it < kTreesPerWarp; it++) {
-                const int slot = warp + kWarps * it;
+            for (int it = 0; it < kTile / kWarps; it++) {
+                const int slot = (it / TPW) * (kWarps * TPW) + warp * TPW + (it % TPW);
                 const int b = tile * kTile + slot;
                 if (b >= tr.batch) break;
-                EmitRec<NPL> &er = rec[slot];
+                EmitRec<G> &er = rec[slot];
                 const int k = er.k;
                 uint32_t st = er.status;
-                TreeState<NPL> t;
-                t.n = er.n;
+                uint64_t keep[W];
 #pragma unroll
-                for (int w = 0; w < W; w++) t.keep[w] = er.keep[w];
-                if (k > 0) tree_fill_klist<NPL>(t, sm);
-                tree_union<NPL, IDF, KT, EW, CL>(st, sm, k, b, N, rt.num_layers, rt.top_k,
-                                                 rt.num_experts, rt.id_format, rt.ids, flags, Epad,
-                                                 out.union_count, out.union_total, out.union_bits,
-                                                 out.expert_hist);
+                for (int w = 0; w < W; w++) keep[w] = er.keep[w];
+                for (int i = lane; i < er.n; i += 32)
+                    if (grp::bit_w<W>(keep, i)) klist[grp::popc_below_w<W>(keep, i)] = (uint8_t)i;
+                __syncwarp();
+                tree_union<NPL, IDF, KT, EW, CL>(st, klist, k, b, N, L, rt.top_k, E, rt.id_format,
+                                                 rt.ids, wscr, Epad, out.union_count, out.union_total,
+                                                 out.union_bits, out.expert_hist);
                 if (lane == 0) er.status = st;
+                __syncwarp();
             }
         }
         // ---------------- look-back for the tile prefix + next ticket
@@ -433,38 +462,76 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_fused(evict_trees_t tr, cons
         }
         __syncthreads();
         const int next = s_tile;
-        // ---------------- phase C: verify-tree build per tree
+        // ---------------- C: verify-tree emit, sub-warp per tree
 #pragma unroll 1
-        for (int it = 0; it < kTreesPerWarp; it++) {
-            const int slot = warp + kWarps * it;
+        for (int pass = 0; pass < PASSES; pass++) {
+            const int slot = pass * (kWarps * TPW) + warp * TPW + gi;
             const int b = tile * kTile + slot;
-            if (b >= tr.batch) break;
-            const EmitRec<NPL> &er = rec[slot];
-            const int k = er.k;
+            const bool active = b < tr.batch;
+            const EmitRec<G> &er = rec[slot];
+            const int k = active ? er.k : 0;
             const int off = s_off[slot];
-            if (lane == 0 && out.status) out.status[b] = er.status;
-            if (lane == 0 && out.verify_offsets) {
-                out.verify_offsets[b] = off;
-                if (b == tr.batch - 1) out.verify_offsets[tr.batch] = off + k;
-            }
-            if (k > 0) {
-                TreeState<NPL> t;
-                t.n = er.n;
-#pragma unroll
-                for (int r = 0; r < NPL; r++) {
-                    t.par[r] = er.par[base + r];
-                    t.dep[r] = er.dep[base + r];
+            if (active && g == 0) {
+                if (out.status) out.status[b] = er.status;
+                if (out.verify_offsets) {
+                    out.verify_offsets[b] = off;
+                    if (b == tr.batch - 1) out.verify_offsets[tr.batch] = off + k;
                 }
-#pragma unroll
-                for (int w = 0; w < W; w++) t.keep[w] = er.keep[w];
-                tree_build_emit<NPL>(t, sm, k, b, N, off,
-                                     out.pos_offset ? __ldg(out.pos_offset + b) : 0, out.kept_index,
-                                     out.retrieve_index, out.positions, out.next_token,
-                                     out.next_sibling, out.tree_mask);
             }
+            uint64_t keep[W];
+#pragma unroll
+            for (int w = 0; w < W; w++) keep[w] = active ? er.keep[w] : 0ull;
+            uint64_t *child = reinterpret_cast<uint64_t *>(wscr) + (size_t)gi * NMAX * W;
+            grp::g_emit<G>(keep, active ? er.n : 0, active && k > 0, k, b, N, off,
+                           (active && out.pos_offset) ? __ldg(out.pos_offset + b) : 0, er.par, er.dep,
+                           child, out.kept_index, out.retrieve_index, out.positions, out.next_token,
+                           out.next_sibling, out.tree_mask);
+            __syncwarp();
         }
         tile = next;
     }
+}
+
+// ------------------------------------------------------------ select (grouped)
+// evict_select: G lanes per tree, 32/G trees per warp, 4 warps per CTA (small
+// CTAs keep batch-64 latency low: 64 trees → 4 CTAs on 4 SMs).
+constexpr int kSelWarps = 4;
+
+template <int G>
+__global__ void __launch_bounds__(kSelWarps * 32) k_select_g(evict_trees_t tr, const float *cost,
+                                                             int cost_stride, int32_t *k_star,
+                                                             float *e_hat, float *utility,
+                                                             uint64_t *keep_bits, int32_t *order,
+                                                             float *prefix_sums, uint32_t *status)
+{
+    constexpr int TPW = grp::GShape<G>::TPW;
+    constexpr int NMAX = grp::GShape<G>::NMAX;
+    constexpr int W = grp::GShape<G>::W;
+    __shared__ __align__(16) int2 sd_all[kSelWarps * TPW * NMAX];
+    __shared__ uint8_t rk_all[kSelWarps * TPW * NMAX];
+    const int warp = threadIdx.x >> 5;
+    const int gi = grp::gidx<G>(), g = grp::gl<G>();
+    const int slot = warp * TPW + gi;
+    const int b = blockIdx.x * (kSelWarps * TPW) + slot;
+    const bool active = b < tr.batch;
+    const int N = tr.max_nodes;
+    const int WN = (N + 63) / 64;
+    grp::GTree<G> t;
+    grp::g_load<G>(t, tr.parent, tr.q, tr.n_nodes, b, N, active);
+    float c[grp::NP];
+    grp::g_load_cost<G>(c, t, cost + (size_t)(active ? b : 0) * cost_stride);
+    grp::g_levels<G, true>(t, sd_all + slot * NMAX);
+    int32_t *orow = (active && order) ? order + (size_t)b * N : nullptr;
+    float *prow = (active && prefix_sums) ? prefix_sums + (size_t)b * N : nullptr;
+    grp::g_rank_argmax<G>(t, rk_all + slot * NMAX, c, N, orow, prow);
+    if (!active) return;
+    if (g == 0) {
+        k_star[b] = t.kstar;
+        e_hat[b] = t.ehat;
+        utility[b] = t.util;
+        if (status) status[b] = t.status;
+    }
+    if (g < WN) keep_bits[(size_t)b * WN + g] = t.keep[g < W ? g : 0];
 }
 
 // ------------------------------------------------------------ launchers
@@ -528,7 +595,8 @@ struct UnionLauncher {
                               cudaStream_t s)
     {
         const int blocks = (tr->batch + kWarps - 1) / kWarps;
-        const size_t dyn = (IDF == 1 || IDF == 4) ? (size_t)kWarps * rt->num_layers * union_epad(rt->num_experts) : 0;
+        const size_t dyn = (IDF == 1 || IDF == 4) ? (size_t)kWarps * 16 * union_epad_u(rt->num_experts) *
+                                                        ((2 * rt->num_layers + 31) / 32) : 0;
         auto kern = k_union<NPL, IDF, KT, EW, CL>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         kern<<<blocks, kWarps * 32, dyn, s>>>(*tr, keep, *rt, uc, ut, ub, eh, st);
@@ -543,9 +611,9 @@ struct FusedLauncher {
                               int ntiles, cudaStream_t s)
     {
         auto kern = k_fused<NPL, IDF, KT, EW, CL>;
-        const size_t dyn = fused_flags_offset<NPL>() +
-                           ((IDF == 1 || IDF == 4) && o->union_count
-                                ? (size_t)kWarps * rt->num_layers * union_epad(rt->num_experts) : 0);
+        constexpr int G = NPL == 2 ? 8 : 16;
+        const size_t dyn = fused_smem_bytes<G>(rt->num_layers, rt->num_experts,
+                                               (IDF == 1 || IDF == 4) && o->union_count);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         const int blocks = persistent_blocks(kern, ntiles, dyn);
         kern<<<blocks, kWarps * 32, dyn, s>>>(*tr, cost, cs, *rt, *o, ws, ntiles);
@@ -558,9 +626,19 @@ evict_status_t launch_select(const evict_trees_t *tr, const float *cost, int cs,
                              float *e_hat, float *utility, uint64_t *keep_bits, int32_t *order,
                              float *prefix_sums, uint32_t *status, cudaStream_t s)
 {
-    const int blocks = (tr->batch + kWarps - 1) / kWarps;
-    k_select<NPL><<<blocks, kWarps * 32, 0, s>>>(*tr, cost, cs, k_star, e_hat, utility, keep_bits,
-                                                   order, prefix_sums, status);
+    if (tr->batch <= 4096) {
+        // latency regime (serving batches): one warp per tree, shortest dependency chain
+        const int blocks = (tr->batch + kWarps - 1) / kWarps;
+        k_select<NPL><<<blocks, kWarps * 32, 0, s>>>(*tr, cost, cs, k_star, e_hat, utility, keep_bits,
+                                                       order, prefix_sums, status);
+        return launched();
+    }
+    // throughput regime: sub-warp groups, 32/G trees per warp instruction
+    constexpr int G = NPL == 2 ? 8 : 16;
+    constexpr int per_cta = kSelWarps * grp::GShape<G>::TPW;
+    const int blocks = (tr->batch + per_cta - 1) / per_cta;
+    k_select_g<G><<<blocks, kSelWarps * 32, 0, s>>>(*tr, cost, cs, k_star, e_hat, utility, keep_bits,
+                                                      order, prefix_sums, status);
     return launched();
 }
 

@@ -508,7 +508,7 @@ __device__ __forceinline__ void or_ids_u8x4(LayerBits<EW> &bs, uint32_t wv, uint
 // IDF: 1 = u8 ids, 4 = i32 ids, 8 = masks.  KT: compile-time K (0 = runtime).
 // Generic layout: lane `lane` owns layers l = lane + 32c (any K, any E ≤ 256).
 template <int NPL, int IDF, int KT, int EW, int CL>
-__device__ __forceinline__ void tree_union_generic(uint32_t &status, const WarpSlab<NPL> &sm, int k,
+__device__ __forceinline__ void tree_union_generic(uint32_t &status, const uint8_t *__restrict__ klist, int k,
                                            int b, int N, int L, int K, int E, int idb,
                                            const void *__restrict__ ids,
                                            int32_t *__restrict__ union_count,
@@ -532,7 +532,7 @@ __device__ __forceinline__ void tree_union_generic(uint32_t &status, const WarpS
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int j = j0 + u;
-                    const int node = j < k ? sm.klist[j] : 0;
+                    const int node = j < k ? klist[j] : 0;
                     const uint8_t *rowp = (const uint8_t *)ids + ((size_t)b * N + node) * L * 8;
 #pragma unroll
                     for (int c = 0; c < CL; c++) {
@@ -555,7 +555,7 @@ __device__ __forceinline__ void tree_union_generic(uint32_t &status, const WarpS
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int j = j0 + u;
-                    const int node = j < k ? sm.klist[j] : 0;
+                    const int node = j < k ? klist[j] : 0;
                     const int32_t *rowp = (const int32_t *)ids + ((size_t)b * N + node) * L * 8;
 #pragma unroll
                     for (int c = 0; c < CL; c++) {
@@ -586,7 +586,7 @@ __device__ __forceinline__ void tree_union_generic(uint32_t &status, const WarpS
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int j = j0 + u;
-                    const int node = j < k ? sm.klist[j] : 0;
+                    const int node = j < k ? klist[j] : 0;
                     const uint64_t *rowp = (const uint64_t *)ids + ((size_t)b * N + node) * L * EWr;
 #pragma unroll
                     for (int c = 0; c < CL; c++) {
@@ -619,7 +619,7 @@ __device__ __forceinline__ void tree_union_generic(uint32_t &status, const WarpS
                 for (int u = 0; u < U; u++) {
                     const int j = j0 + u;
                     if (j >= k) break;
-                    const int node = sm.klist[j];
+                    const int node = klist[j];
 #pragma unroll
                     for (int c = 0; c < CL; c++) {
                         const int l = lane + 32 * c;
@@ -696,7 +696,7 @@ namespace evict {
 // no lane idles.  Parts of one layer sit in adjacent lanes and are merged with
 // __shfl_xor_sync at the end.  R = register rounds (≥ ceil(L·P/32)).
 template <int NPL, int IDF, int EW, int R>
-__device__ __forceinline__ void tree_union_fast(uint32_t &status, const WarpSlab<NPL> &sm, int k,
+__device__ __forceinline__ void tree_union_fast(uint32_t &status, const uint8_t *__restrict__ klist, int k,
                                                 int b, int N, int L, int E,
                                                 const void *__restrict__ ids,
                                                 int32_t *__restrict__ union_count,
@@ -727,7 +727,7 @@ __device__ __forceinline__ void tree_union_fast(uint32_t &status, const WarpSlab
                 for (int u = 0; u < U; u++) {
                     const int j = j0 + u;
                     const uint32_t *rowp = reinterpret_cast<const uint32_t *>(
-                        (const uint8_t *)ids + ((size_t)b * N + (j < k ? sm.klist[j] : 0)) * row_elems);
+                        (const uint8_t *)ids + ((size_t)b * N + (j < k ? klist[j] : 0)) * row_elems);
 #pragma unroll
                     for (int c = 0; c < R; c++) {
                         const int sl = lane + 32 * c;
@@ -752,7 +752,7 @@ __device__ __forceinline__ void tree_union_fast(uint32_t &status, const WarpSlab
                 for (int u = 0; u < U; u++) {
                     const int j = j0 + u;
                     const int4 *rowp = reinterpret_cast<const int4 *>(
-                        (const int32_t *)ids + ((size_t)b * N + (j < k ? sm.klist[j] : 0)) * row_elems);
+                        (const int32_t *)ids + ((size_t)b * N + (j < k ? klist[j] : 0)) * row_elems);
 #pragma unroll
                     for (int c = 0; c < R; c++) {
                         const int sl = lane + 32 * c;
@@ -780,7 +780,7 @@ __device__ __forceinline__ void tree_union_fast(uint32_t &status, const WarpSlab
                 for (int u = 0; u < U; u++) {
                     const int j = j0 + u;
                     const uint2 *rowp = reinterpret_cast<const uint2 *>(
-                        (const uint64_t *)ids + ((size_t)b * N + (j < k ? sm.klist[j] : 0)) * row_elems);
+                        (const uint64_t *)ids + ((size_t)b * N + (j < k ? klist[j] : 0)) * row_elems);
 #pragma unroll
                     for (int c = 0; c < R; c++) {
                         const int sl = lane + 32 * c;
@@ -874,29 +874,36 @@ __device__ __forceinline__ void tree_union_fast(uint32_t &status, const WarpSlab
     if (union_total && lane == 0) union_total[b] = tot;
 }
 
-// Top-8 ids (u8 or i32) via per-warp shared-memory expert flags: the union of
-// a layer is the set of flag bytes written.  Each id costs one byte store
-// (a warp store covers 32 ids, no read-modify-write, duplicate ids are
-// idempotent), instead of building one-hot words in registers.  The flag
-// region of the warp is [L][Epad] bytes (Epad = E rounded up to 128); a layer
-// splits into two halves owned by adjacent lanes (slot = 2l + half), which
-// count (popc of 0/1 bytes), optionally pack bits, and clear their half.
-template <int NPL, int IDF, int R>
-__device__ __forceinline__ void tree_union_flags(uint32_t &status, const WarpSlab<NPL> &sm, int k,
-                                                 int b, int N, int L, int E,
+// Top-8 ids (u8 or i32) via per-warp shared-memory expert flags.  A layer's
+// 8 ids split into two 4-id halves; slot = 2l + half; lane `lane` owns slots
+// lane + 32c (round c < R, 16 layers per round).  In round c's flag block the
+// byte of (layer j' = lane/2, expert e) lives in 32-bit word (e/4)·16 + j' at
+// byte e%4, so a store's bank is 16·((e/4)&1) + j': lanes of different layers
+// never collide, only the two halves of one layer can (half the time).  One
+// byte store per id (no read-modify-write, duplicates idempotent); then each
+// lane counts its half (popc of 0/1 bytes), optionally packs the bits, and
+// clears its words.  Region: R·Epad·16 bytes per warp.
+template <int NPL, int IDF, int R, bool E128, bool BITS>
+__device__ __forceinline__ void tree_union_flags(uint32_t &status, const uint8_t *__restrict__ klist,
+                                                 int k, int b, int N, int L, int E,
                                                  const void *__restrict__ ids, uint8_t *flags,
                                                  int Epad, int32_t *__restrict__ union_count,
                                                  int32_t *__restrict__ union_total,
-                                                 uint64_t *__restrict__ union_bits,
-                                                 int64_t *__restrict__ expert_hist)
+                                                 uint64_t *__restrict__ union_bits)
 {
     const int lane = lane_id();
     const int S = 2 * L;
+    const int jp = lane >> 1, h = lane & 1;
+    const int blk = Epad * 16;                      // bytes per round block
+    const int G4 = Epad >> 2;                       // flag words per layer
+    const int HW = G4 >> 1;                         // words per half
+    const int EWr = (E + 63) >> 6;
+    const size_t row = (size_t)L * 8;               // ids per node row
+    const uint8_t *tree_u8 = (const uint8_t *)ids + (size_t)b * N * row;
+    const int32_t *tree_i32 = (const int32_t *)ids + (size_t)b * N * row;
     uint32_t bad = 0;
-    if (!status) {
-        const size_t row = (size_t)L * 8;                  // ids per node row
-        const uint8_t *tree_u8 = (const uint8_t *)ids + (size_t)b * N * row;
-        const int32_t *tree_i32 = (const int32_t *)ids + (size_t)b * N * row;
+    const bool run = status == 0;
+    if (run) {
         constexpr int U = 4;
         for (int j0 = 0; j0 < k; j0 += U) {
             if constexpr (IDF == 1) {
@@ -905,7 +912,7 @@ __device__ __forceinline__ void tree_union_flags(uint32_t &status, const WarpSla
                 for (int u = 0; u < U; u++) {
                     const int j = j0 + u;
                     const uint32_t *rowp = reinterpret_cast<const uint32_t *>(
-                        tree_u8 + (uint32_t)(j < k ? sm.klist[j] : 0) * (uint32_t)row);
+                        tree_u8 + (uint32_t)(j < k ? klist[j] : 0) * (uint32_t)row);
 #pragma unroll
                     for (int c = 0; c < R; c++) {
                         const int sl = lane + 32 * c;
@@ -916,19 +923,23 @@ __device__ __forceinline__ void tree_union_flags(uint32_t &status, const WarpSla
                 for (int u = 0; u < U; u++)
 #pragma unroll
                     for (int c = 0; c < R; c++) {
-                        const int sl = lane + 32 * c;
-                        if (j0 + u < k && sl < S) {
-                            uint8_t *fl = flags + (sl >> 1) * Epad;
-                            const uint32_t wv = v[u][c];
-                            if (E == 128) {
+                        if (j0 + u < k && lane + 32 * c < S) {
+                            uint8_t *fl = flags + c * blk + jp * 4;
+                            uint32_t wv = v[u][c];
+                            if constexpr (E128) {
                                 bad |= wv & 0x80808080u;
+                                wv &= 0x7F7F7F7Fu;
 #pragma unroll
-                                for (int q = 0; q < 4; q++) fl[__byte_perm(wv, 0, 0x4440 | q) & 127u] = 1;
+                                for (int q = 0; q < 4; q++) {
+                                    const uint32_t e = __byte_perm(wv, 0, 0x4440 | q);
+                                    fl[e * 16u - (e & 3u) * 15u] = 1;
+                                }
                             } else {
 #pragma unroll
                                 for (int q = 0; q < 4; q++) {
                                     const uint32_t e = __byte_perm(wv, 0, 0x4440 | q);
-                                    if (e < (uint32_t)E) fl[e] = 1; else bad = 1;
+                                    if (e < (uint32_t)E) fl[e * 16u - (e & 3u) * 15u] = 1;
+                                    else bad = 1;
                                 }
                             }
                         }
@@ -939,7 +950,7 @@ __device__ __forceinline__ void tree_union_flags(uint32_t &status, const WarpSla
                 for (int u = 0; u < U; u++) {
                     const int j = j0 + u;
                     const int4 *rowp = reinterpret_cast<const int4 *>(
-                        tree_i32 + (uint32_t)(j < k ? sm.klist[j] : 0) * (uint32_t)row);
+                        tree_i32 + (uint32_t)(j < k ? klist[j] : 0) * (uint32_t)row);
 #pragma unroll
                     for (int c = 0; c < R; c++) {
                         const int sl = lane + 32 * c;
@@ -950,76 +961,60 @@ __device__ __forceinline__ void tree_union_flags(uint32_t &status, const WarpSla
                 for (int u = 0; u < U; u++)
 #pragma unroll
                     for (int c = 0; c < R; c++) {
-                        const int sl = lane + 32 * c;
-                        if (j0 + u < k && sl < S) {
-                            uint8_t *fl = flags + (sl >> 1) * Epad;
+                        if (j0 + u < k && lane + 32 * c < S) {
+                            uint8_t *fl = flags + c * blk + jp * 4;
                             const uint32_t e4[4] = {(uint32_t)v[u][c].x, (uint32_t)v[u][c].y,
                                                     (uint32_t)v[u][c].z, (uint32_t)v[u][c].w};
 #pragma unroll
                             for (int q = 0; q < 4; q++) {
-                                if (e4[q] < (uint32_t)E) fl[e4[q]] = 1; else bad = 1;
+                                const uint32_t e = e4[q];
+                                if (e < (uint32_t)E) fl[e * 16u - (e & 3u) * 15u] = 1;
+                                else bad = 1;
                             }
                         }
                     }
             }
         }
-        if (__any_sync(kFull, bad)) status |= EVICT_TREE_BAD_EXPERT;
     }
     __syncwarp();
+    const bool anybad = run && __any_sync(kFull, bad);
+    if (anybad) status |= EVICT_TREE_BAD_EXPERT;
     const bool zero = status != 0;
-    const bool want_bits = union_bits != nullptr || expert_hist != nullptr;
-    const int half = Epad >> 1;                       // bytes (= experts) per half, multiple of 64
-    const int EWr = (E + 63) >> 6;
     int tot = 0;
 #pragma unroll
     for (int c = 0; c < R; c++) {
         const int sl = lane + 32 * c;
         const bool in = sl < S;
-        const int l = sl >> 1, h = sl & 1;
+        const int l = sl >> 1;
+        const uint32_t *fw = reinterpret_cast<const uint32_t *>(flags + c * blk);
+        uint32_t *fwm = reinterpret_cast<uint32_t *>(flags + c * blk);
         int cnt = 0;
-        uint64_t bits[2] = {0ull, 0ull};              // half ≤ 128 experts
-        if (in) {
-            uint4 *fp = reinterpret_cast<uint4 *>(flags + l * Epad + h * half);
-            for (int q = 0; q < (half >> 4); q++) {
-                const uint4 x = fp[q];
-                cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
-                if (want_bits) {
-                    const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-                    for (int m = 0; m < 4; m++) {
-                        const uint32_t nib = (xs[m] & 1u) | ((xs[m] >> 7) & 2u) | ((xs[m] >> 14) & 4u) |
-                                             ((xs[m] >> 21) & 8u);
-                        const int pos = q * 16 + m * 4;
-                        bits[pos >> 6] |= (uint64_t)nib << (pos & 63);
-                    }
+        uint64_t bits[2] = {0ull, 0ull};
+        if (run && in) {        // flags were written only for good-status trees
+            for (int qq = 0; qq < HW; qq++) {
+                const int g = h * HW + ((qq + h) & (HW - 1));   // rotated: halves hit different banks
+                const uint32_t x = fw[g * 16 + jp];
+                cnt += __popc(x);
+                if constexpr (BITS) {
+                    const uint32_t nib = (x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u);
+                    const int pos = (g - h * HW) * 4;
+                    bits[pos >> 6] |= (uint64_t)nib << (pos & 63);
                 }
-                fp[q] = make_uint4(0u, 0u, 0u, 0u);
+                fwm[g * 16 + jp] = 0u;
             }
         }
         cnt += __shfl_xor_sync(kFull, cnt, 1);
-        if (zero) {
-            cnt = 0;
-            bits[0] = bits[1] = 0ull;
-        }
         if (!in) continue;
+        if (zero) { cnt = 0; bits[0] = bits[1] = 0ull; }
         if (h == 0) {
             union_count[(size_t)b * L + l] = cnt;
             tot += cnt;
         }
-        const int w0 = h * (half >> 6);               // first 64-bit word of this half
+        if constexpr (BITS) {
+            const int w0 = h * (HW >> 4);                // first 64-bit word of this half
 #pragma unroll
-        for (int w = 0; w < 2; w++) {
-            if (w < (half >> 6) && w0 + w < EWr) {
-                if (union_bits) union_bits[((size_t)b * L + l) * EWr + w0 + w] = bits[w];
-                if (expert_hist && !zero) {
-                    uint64_t mm = bits[w];
-                    while (mm) {
-                        const int e = (w0 + w) * 64 + __ffsll((long long)mm) - 1;
-                        mm &= mm - 1;
-                        atomicAdd(reinterpret_cast<unsigned long long *>(expert_hist + (size_t)l * E + e), 1ull);
-                    }
-                }
-            }
+            for (int w = 0; w < 2; w++)
+                if (w < (HW >> 4) && w0 + w < EWr) union_bits[((size_t)b * L + l) * EWr + w0 + w] = bits[w];
         }
     }
     __syncwarp();
@@ -1029,7 +1024,7 @@ __device__ __forceinline__ void tree_union_flags(uint32_t &status, const WarpSla
 
 // Dispatch: flags for top-8 ids, register OR for 1/2/4-word masks, generic otherwise.
 template <int NPL, int IDF, int KT, int EW, int R>
-__device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL> &sm, int k, int b,
+__device__ __forceinline__ void tree_union(uint32_t &status, const uint8_t *__restrict__ klist, int k, int b,
                                            int N, int L, int K, int E, int idb,
                                            const void *__restrict__ ids, uint8_t *flags, int Epad,
                                            int32_t *__restrict__ union_count,
@@ -1037,14 +1032,31 @@ __device__ __forceinline__ void tree_union(uint32_t &status, const WarpSlab<NPL>
                                            uint64_t *__restrict__ union_bits,
                                            int64_t *__restrict__ expert_hist)
 {
-    if constexpr (IDF == 1 || IDF == 4)
-        tree_union_flags<NPL, IDF, R>(status, sm, k, b, N, L, E, ids, flags, Epad, union_count,
-                                      union_total, union_bits, expert_hist);
+    if constexpr (IDF == 1 || IDF == 4) {
+        if (expert_hist == nullptr) {   // the flag path cannot retract a bad tree's histogram rows
+            const bool e128 = IDF == 1 && E == 128;
+            if (union_bits == nullptr) {
+                if (e128) tree_union_flags<NPL, IDF, R, true, false>(status, klist, k, b, N, L, E, ids, flags,
+                                                                      Epad, union_count, union_total, nullptr);
+                else tree_union_flags<NPL, IDF, R, false, false>(status, klist, k, b, N, L, E, ids, flags,
+                                                                 Epad, union_count, union_total, nullptr);
+            } else {
+                if (e128) tree_union_flags<NPL, IDF, R, true, true>(status, klist, k, b, N, L, E, ids, flags,
+                                                                     Epad, union_count, union_total, union_bits);
+                else tree_union_flags<NPL, IDF, R, false, true>(status, klist, k, b, N, L, E, ids, flags,
+                                                                Epad, union_count, union_total, union_bits);
+            }
+        } else {
+            tree_union_generic<NPL, IDF, KT, EW, (R + 1) / 2>(status, klist, k, b, N, L, K, E, idb, ids,
+                                                             union_count, union_total, union_bits,
+                                                             expert_hist);
+        }
+    }
     else if constexpr (IDF == 8)
-        tree_union_fast<NPL, IDF, EW, R>(status, sm, k, b, N, L, E, ids, union_count, union_total,
+        tree_union_fast<NPL, IDF, EW, R>(status, klist, k, b, N, L, E, ids, union_count, union_total,
                                          union_bits, expert_hist);
     else
-        tree_union_generic<NPL, IDF, KT, EW, R / 2>(status, sm, k, b, N, L, K, E, idb, ids,
+        tree_union_generic<NPL, IDF, KT, EW, R / 2>(status, klist, k, b, N, L, K, E, idb, ids,
                                                     union_count, union_total, union_bits, expert_hist);
 }
 

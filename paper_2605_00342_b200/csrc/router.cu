@@ -4,7 +4,9 @@
 // One CTA = (layer l, 128 packed verify rows).  D[128 rows][128 experts] =
 // H·W_gᵀ accumulates in TMEM (128 fp32 columns) over d in 64-wide k-blocks:
 //   warps 0–3  gather the rows' hidden states (cp.async, 16 B per thread,
-//              128-byte XOR swizzle) into a 6-stage ring, then run the
+//              128-byte XOR swizzle) into a 6-stage ring, arriving on the
+//              stage barrier asynchronously (cp.async.mbarrier.arrive.noinc),
+//              then run the
 //              epilogue: tcgen05.ld → per-row TopK (logit desc, expert asc)
 //              → warp-aggregated atomicOr into the tree's union bitset
 //   warp 4     one elected thread issues tcgen05.mma (M128 N128 K16, bf16 →
@@ -71,6 +73,10 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar)
+{
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -129,7 +135,15 @@ struct Params {
     unsigned long long *bits;      // [B][L][2]
     int32_t *topk_ids;             // [L][B*N][K] or null
     float *dbg_logits;             // [L][B*N][128] or null (debug entry point only)
+    long long *trace;              // [256] globaltimer trace of CTA (0,0) or null (debug only)
 };
+
+__device__ __forceinline__ long long gtimer()
+{
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 __global__ void __launch_bounds__(THREADS, 1)
 k_router(const __grid_constant__ CUtensorMap wmap, Params p)
@@ -150,6 +164,8 @@ k_router(const __grid_constant__ CUtensorMap wmap, Params p)
     auto A = [&](int s) { return base_u32 + s * STAGE_BYTES; };
     auto Bs = [&](int s) { return base_u32 + s * STAGE_BYTES + A_BYTES; };
 
+    const bool tr0 = p.trace && blockIdx.x == 0 && blockIdx.y == 0;
+    if (tr0 && threadIdx.x == 0) p.trace[250] = gtimer();
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(full0 + 8 * s, NPROD + 1);
@@ -180,6 +196,7 @@ k_router(const __grid_constant__ CUtensorMap wmap, Params p)
         for (int kb = 0; kb < KB; kb++) {
             const int s = kb % STAGES;
             if (kb >= STAGES) mbar_wait(empty0 + 8 * s, ((kb / STAGES) - 1) & 1);
+            if (tr0 && threadIdx.x == 0 && kb < 64) p.trace[128 + kb] = gtimer();
 #pragma unroll
             for (int j = 0; j < 8; j++) {
                 const int row = r0 + 16 * j;
@@ -187,23 +204,34 @@ k_router(const __grid_constant__ CUtensorMap wmap, Params p)
                 const uint16_t *src = hl + (size_t)(rid < 0 ? 0 : rid) * p.d + kb * BK + c * 8;
                 cp_async16(A(s) + row * 128 + ((c ^ (row & 7)) << 4), src, rid < 0 ? 0u : 16u);
             }
-            cp_async_commit();
-            if (kb >= STAGES - 1) {
-                cp_async_wait<STAGES - 1>();
-                fence_proxy_async();
-                mbar_arrive(full0 + 8 * ((kb - (STAGES - 1)) % STAGES));
-            }
+            // arrive on full[s] asynchronously once this thread's copies have landed:
+            // the producer never blocks on its own loads, only on slot reuse (empty[s])
+            cp_async_arrive_noinc(full0 + 8 * s);
         }
         cp_async_wait<0>();
-        fence_proxy_async();
-        for (int kb = (KB > STAGES - 1 ? KB - (STAGES - 1) : 0); kb < KB; kb++) mbar_arrive(full0 + 8 * (kb % STAGES));
 
         // ---- epilogue: TMEM → registers → TopK → union bits
+        if (tr0 && threadIdx.x == 0) p.trace[192] = gtimer();
         mbar_wait(tfull, 0);
+        if (tr0 && threadIdx.x == 0) p.trace[193] = gtimer();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int row = warp * 32 + lane;
         const int r = m0 + row;
         const bool valid = r < T;
+        // stage the row's 128 logits in shared memory (the operand ring is free now;
+        // stride 129 floats: thread t's element i sits in bank (t + i) % 32), then run a
+        // compact, non-unrolled TopK scan over them (a fully unrolled register scan
+        // overflows the instruction cache)
+        float *lg = reinterpret_cast<float *>(base) + (size_t)row * (BN + 1);
+#pragma unroll 1
+        for (int chunk = 0; chunk < BN / 32; chunk++) {
+            float v[32];
+            tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + chunk * 32, v);
+#pragma unroll
+            for (int i = 0; i < 32; i++) lg[chunk * 32 + i] = v[i];
+            if (p.dbg_logits && valid)
+                for (int i = 0; i < 32; i++) p.dbg_logits[((size_t)l * BNrows + r) * BN + chunk * 32 + i] = v[i];
+        }
         float bv[KMAX];
         int bi[KMAX];
 #pragma unroll
@@ -211,40 +239,39 @@ k_router(const __grid_constant__ CUtensorMap wmap, Params p)
         float thr = bv[0];
         const int K = p.K;
 #pragma unroll 1
-        for (int chunk = 0; chunk < BN / 32; chunk++) {
-            float v[32];
-            tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + chunk * 32, v);
-            if (p.dbg_logits && valid)
-                for (int i = 0; i < 32; i++) p.dbg_logits[((size_t)l * BNrows + r) * BN + chunk * 32 + i] = v[i];
+        for (int i = 0; i < BN; i++) {
+            const float vi = lg[i];
+            if (vi > thr) {                       // later experts never beat equal logits
+                float cv = vi;
+                int ci = i;
 #pragma unroll
-            for (int i = 0; i < 32; i++) {
-                if (v[i] > thr) {                 // later experts never beat equal logits
-                    float cv = v[i];
-                    int ci = chunk * 32 + i;
-#pragma unroll
-                    for (int j = 0; j < KMAX; j++) {
-                        if (j < K) {
-                            // full key (logit desc, expert asc): a displaced entry
-                            // keeps its place ahead of an equal logit with a larger id
-                            const bool sw = cv > bv[j] || (cv == bv[j] && ci < bi[j]);
-                            const float tv = bv[j];
-                            const int ti = bi[j];
-                            bv[j] = sw ? cv : tv;
-                            bi[j] = sw ? ci : ti;
-                            cv = sw ? tv : cv;
-                            ci = sw ? ti : ci;
-                        }
+                for (int j = 0; j < KMAX; j++) {
+                    if (j < K) {
+                        // full key (logit desc, expert asc): a displaced entry
+                        // keeps its place ahead of an equal logit with a larger id
+                        const bool sw = cv > bv[j] || (cv == bv[j] && ci < bi[j]);
+                        const float tv = bv[j];
+                        const int ti = bi[j];
+                        bv[j] = sw ? cv : tv;
+                        bi[j] = sw ? ci : ti;
+                        cv = sw ? tv : cv;
+                        ci = sw ? ti : ci;
                     }
-#pragma unroll
-                    for (int j = 0; j < KMAX; j++)
-                        if (j == K - 1) thr = bv[j];
                 }
+#pragma unroll
+                for (int j = 0; j < KMAX; j++)
+                    if (j == K - 1) thr = bv[j];
             }
         }
         uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int j = 0; j < KMAX; j++)
-            if (j < K && bi[j] < BN) w[bi[j] >> 5] |= 1u << (bi[j] & 31);
+        for (int j = 0; j < KMAX; j++) {
+            if (j < K && bi[j] < BN) {
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    if ((bi[j] >> 5) == q) w[q] |= 1u << (bi[j] & 31);
+            }
+        }
         if (valid && p.topk_ids) {
 #pragma unroll
             for (int j = 0; j < KMAX; j++)
@@ -273,6 +300,7 @@ k_router(const __grid_constant__ CUtensorMap wmap, Params p)
             for (int kb = 0; kb < KB; kb++) {
                 const int s = kb % STAGES;
                 mbar_wait(full0 + 8 * s, (kb / STAGES) & 1);
+                if (tr0 && kb < 64) p.trace[kb] = gtimer();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                 for (int k = 0; k < BK / 16; k++)
@@ -288,14 +316,17 @@ k_router(const __grid_constant__ CUtensorMap wmap, Params p)
             for (int kb = 0; kb < KB; kb++) {
                 const int s = kb % STAGES;
                 if (kb >= STAGES) mbar_wait(empty0 + 8 * s, ((kb / STAGES) - 1) & 1);
+                if (tr0 && kb < 64) p.trace[64 + kb] = gtimer();
                 mbar_arrive_tx(full0 + 8 * s, B_BYTES);
                 tma_load_2d(Bs(s), &wmap, full0 + 8 * s, kb * BK, l * BN);
             }
         }
         __syncwarp();
     }
+    if (tr0 && threadIdx.x == 0) p.trace[194] = gtimer();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (tr0 && threadIdx.x == 0) p.trace[195] = gtimer();
     if (warp == 4) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
@@ -344,7 +375,7 @@ using namespace evict::router;
 static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *verify_offsets,
                                   const int32_t *retrieve_index, const evict_router_t *rt,
                                   int32_t *union_count, int32_t *union_total, uint64_t *union_bits,
-                                  int32_t *topk_ids, float *dbg_logits, void *stream);
+                                  int32_t *topk_ids, float *dbg_logits, long long *trace, void *stream);
 
 extern "C" evict_status_t evict_router_union(const evict_trees_t *trees, const int32_t *verify_offsets,
                                              const int32_t *retrieve_index, const evict_router_t *rt,
@@ -352,7 +383,7 @@ extern "C" evict_status_t evict_router_union(const evict_trees_t *trees, const i
                                              uint64_t *union_bits, int32_t *topk_ids, void *stream)
 {
     return router_impl(trees, verify_offsets, retrieve_index, rt, union_count, union_total, union_bits,
-                       topk_ids, nullptr, stream);
+                       topk_ids, nullptr, nullptr, stream);
 }
 
 // Debug entry point (not part of include/evict.h): also dumps the raw fp32 logits.
@@ -360,16 +391,16 @@ extern "C" evict_status_t evict_router_union_debug(const evict_trees_t *trees, c
                                                    const int32_t *retrieve_index, const evict_router_t *rt,
                                                    int32_t *union_count, int32_t *union_total,
                                                    uint64_t *union_bits, int32_t *topk_ids, float *logits,
-                                                   void *stream)
+                                                   long long *trace, void *stream)
 {
     return router_impl(trees, verify_offsets, retrieve_index, rt, union_count, union_total, union_bits,
-                       topk_ids, logits, stream);
+                       topk_ids, logits, trace, stream);
 }
 
 static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *verify_offsets,
                                   const int32_t *retrieve_index, const evict_router_t *rt,
                                   int32_t *union_count, int32_t *union_total, uint64_t *union_bits,
-                                  int32_t *topk_ids, float *dbg_logits, void *stream)
+                                  int32_t *topk_ids, float *dbg_logits, long long *trace, void *stream)
 {
     if (!trees || !rt || !verify_offsets || !retrieve_index || !union_count || !union_bits)
         return EVICT_ERR_INVALID_ARG;
@@ -406,6 +437,7 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     p.bits = reinterpret_cast<unsigned long long *>(union_bits);
     p.topk_ids = topk_ids;
     p.dbg_logits = dbg_logits;
+    p.trace = trace;
     dim3 grid((unsigned)(((size_t)B * N + BM - 1) / BM), (unsigned)L);
     k_router<<<grid, THREADS, SMEM_BYTES, s>>>(map, p);
     if (cudaGetLastError() != cudaSuccess) return EVICT_ERR_CUDA;

@@ -312,3 +312,19 @@ def test_batch_stats(ev):
     assert (s.cpu().numpy() == so).all()
     assert np.allclose(d.cpu().numpy(), do, rtol=1e-9)
     assert so[4] == 1
+
+
+@pytest.mark.parametrize("N,steps", [(60, 6), (128, 8)])
+def test_select_large_batch_grouped_kernel(ev, N, steps):
+    """B > 4096 takes the sub-warp (grouped) select kernel; ragged trees and a few adversarial rows."""
+    B = 6000
+    P, Q, n = gen.trees(91, B, N, steps, 10)
+    rng = np.random.default_rng(N)
+    n[::5] = np.maximum(1, (n[::5] * rng.uniform(0.1, 1.0, len(n[::5]))).astype(np.int32))
+    Q[7, 1:] = 1.0                                        # q = 1 ties
+    Q[8, 3] = np.nan                                      # bad prob
+    C = np.tile(gen.cost_table(N), (B, 1))
+    C[9::50, 2::3] = np.inf
+    g = run_select(ev, P, Q, n, C.astype(np.float32), cost_stride=N)
+    o = oracle.select(P, Q, C, n_nodes=n, cost_stride=N, threads=8)
+    check_select(o, g, n)
