@@ -293,6 +293,7 @@ def mask_variant(ev, gen, torch, P, Q, n, cost, ids8, M, stream, reps):
     del call, masks
     torch.cuda.empty_cache()
     return {"id_format": "mask", "value": M / (ms / 1e3), "unit": "trees/s", "kernel_ms": ms,
+            "k_sum": k_sum, "n_sum": n_sum,
             "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "algorithmic_bytes_per_launch": abytes}}
 

@@ -93,7 +93,7 @@ typedef struct {
  *   S[k]     = Σ_{j<k} Score(order[j]) = Ê[A(T_k)] (Eq. 8), fp32.
  *   k*       = smallest argmax_{1≤k≤n_b} S[k]/C(k) (Eq. 10; Z2, Z3).
  * cost: fp32 C(k) at cost[k-1], k = 1..N, per tree at cost + b*cost_stride
- *   (cost_stride 0 = one shared table).  C(k) ∈ (0, +inf]; +inf marks an
+ *   (cost_stride 0 = one shared table); 16-byte aligned, cost_stride % 4 == 0.  C(k) ∈ (0, +inf]; +inf marks an
  *   infeasible k (no verify graph of that length, Z10); cost[0] finite.
  * Outputs: k_star [B] (0 on error), e_hat [B] = S[k*], utility [B] =
  *   S[k*]/C(k*) (C_AR dropped, Z18), keep_bits [B][W] = order[0..k*).

@@ -96,6 +96,7 @@ evict_status_t evict_select(const evict_trees_t *trees, const float *cost, int32
     evict_status_t rc = check_trees(trees);
     if (rc) return rc;
     if (!cost || !k_star || !e_hat || !utility || !keep_bits || cost_stride < 0) return EVICT_ERR_INVALID_ARG;
+    if (((uintptr_t)cost & 15) || (cost_stride % 4)) return EVICT_ERR_INVALID_ARG;
     if ((order == nullptr) != (prefix_sums == nullptr)) return EVICT_ERR_INVALID_ARG;
     if (!dev_info().ok) return EVICT_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
@@ -156,6 +157,7 @@ evict_status_t evict_select_build_union(const evict_trees_t *trees, const float 
     evict_status_t rc = check_trees(trees);
     if (rc) return rc;
     if (!cost || cost_stride < 0 || !out || !workspace) return EVICT_ERR_INVALID_ARG;
+    if (((uintptr_t)cost & 15) || (cost_stride % 4)) return EVICT_ERR_INVALID_ARG;
     if ((out->order == nullptr) != (out->prefix_sums == nullptr)) return EVICT_ERR_INVALID_ARG;
     if (workspace_bytes < evict_workspace_bytes(trees->batch) || ((uintptr_t)workspace & 7))
         return EVICT_ERR_INVALID_ARG;

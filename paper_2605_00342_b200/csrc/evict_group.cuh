@@ -147,18 +147,27 @@ __device__ __forceinline__ void g_load(GTree<G> &t, const int32_t *__restrict__ 
 }
 
 template <int G>
-__device__ __forceinline__ void g_load_cost(float (&c)[NP], GTree<G> &t, const float *__restrict__ cost)
+__device__ __forceinline__ void g_load_cost(float (&c)[NP], GTree<G> &t, const float *__restrict__ cost,
+                                            int N)
 {
     const int base = gl<G>() * NP;
+    // cost rows are 16-byte aligned with N % 4 == 0 (host-checked): two vector loads
+    float4 c0 = make_float4(1.f, 1.f, 1.f, 1.f), c1 = c0;
+    if (!(t.status & EVICT_TREE_BAD_SIZE) && base < t.n) {
+        c0 = __ldg(reinterpret_cast<const float4 *>(cost + base));
+        if (base + 4 < N) c1 = __ldg(reinterpret_cast<const float4 *>(cost + base + 4));
+    }
+    c[0] = c0.x; c[1] = c0.y; c[2] = c0.z; c[3] = c0.w;
+    c[4] = c1.x; c[5] = c1.y; c[6] = c1.z; c[7] = c1.w;
     uint32_t st = 0;
 #pragma unroll
     for (int r = 0; r < NP; r++) {
         const int i = base + r;
-        c[r] = 1.f;
         if (i < t.n && !(t.status & EVICT_TREE_BAD_SIZE)) {
-            c[r] = __ldg(cost + i);
             if (!(c[r] > 0.f)) st |= EVICT_TREE_BAD_COST;
             if (i == 0 && c[r] == __int_as_float(0x7f800000)) st |= EVICT_TREE_BAD_COST;
+        } else {
+            c[r] = 1.f;
         }
     }
     t.status |= g_or<G>(st);
@@ -229,7 +238,9 @@ __device__ __forceinline__ void g_rank_argmax(GTree<G> &t, uint8_t *rk, const fl
         const int i = base + r;
         key[r] = (ok && i < t.n) ? (((uint64_t)(~__float_as_uint(t.sc[r])) << 32) | (uint32_t)i) : ~0ull;
     }
-    // bitonic sort ascending on key == (score desc, index asc); element x = 8g + r
+    // bitonic sort ascending on key == (score desc, index asc); element x = 8g + r.
+    // Valid keys are unique (the index is in the low bits; pads are all ~0), so
+    // a compare-exchange needs one 64-bit comparison: swap ⇔ (a > b) xor desc.
 #pragma unroll
     for (int k = 2; k <= NMAX; k <<= 1) {
 #pragma unroll
@@ -239,21 +250,24 @@ __device__ __forceinline__ void g_rank_argmax(GTree<G> &t, uint8_t *rk, const fl
                 for (int r = 0; r < NP; r++) {
                     const int rp = r ^ j;
                     if (rp > r) {
-                        const bool asc = (((base + r) & k) == 0);
+                        // direction = bit k of x = base + r: base is a multiple of NP, so
+                        // k < NP reads r (compile-time), k ≥ NP reads base (lane-uniform)
+                        const bool desc = (k < NP) ? ((r & k) != 0) : ((base & k) != 0);
                         const uint64_t a = key[r], bb = key[rp];
-                        const bool sw = asc ? (a > bb) : (a < bb);
+                        const bool sw = (a > bb) != desc;
                         key[r] = sw ? bb : a;
                         key[rp] = sw ? a : bb;
                     }
                 }
             } else {
                 const int lj = j / NP;
+                // lane-uniform: lower partner (x & j == 0) keeps the min when ascending
+                const bool take_min = ((base & j) == 0) == ((base & k) == 0);
 #pragma unroll
                 for (int r = 0; r < NP; r++) {
-                    const int x = base + r;
                     const uint64_t o = shfl_xor64(key[r], lj);
-                    const bool take_min = (((x & j) == 0) == ((x & k) == 0));
-                    key[r] = take_min ? (o < key[r] ? o : key[r]) : (o > key[r] ? o : key[r]);
+                    const bool lt = o < key[r];
+                    key[r] = (lt == take_min) ? o : key[r];
                 }
             }
         }
@@ -343,17 +357,20 @@ __device__ __forceinline__ void g_rank_argmax(GTree<G> &t, uint8_t *rk, const fl
 }
 
 // ------------------------------------------------------------ A6
-// Only kept nodes do work: each lane walks the set bits of its 8-node kept
-// mask.  Pass 1 ORs every kept non-root node's slot bit into its parent's
-// child mask (shared atomics); pass 2 builds each kept node's ancestor-or-self
-// row by walking the parent chain in the shared-memory record (depth steps, no
-// level loop) and emits the packed row.  par/dep: the tree's shared record
-// arrays; child: this group's scratch (NMAX × W words).
+// Only kept nodes do work, spread over the group by slot so no lane serialises
+// a cluster of kept nodes (kept nodes crowd the low indices):
+//   1. each lane lists its kept nodes: klist[slot] = node (slot = popc(keep below node));
+//   2. slot s (lane s % G) ORs bit s into its parent's child mask (shared atomics);
+//   3. slot s builds its ancestor-or-self row by walking the parent chain of the
+//      shared-memory record (depth steps, no level loop), reads next-token /
+//      next-sibling from the child masks and emits the packed row.
+// par/dep: the tree's shared record arrays; child (NMAX × W words) and klist
+// (NMAX bytes): this group's scratch.
 template <int G>
 __device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W], int n, bool emit,
                                        int k, int b, int N, int off, int pos_off,
                                        const int8_t *par, const uint8_t *dep, uint64_t *child,
-                                       int32_t *__restrict__ kept_index,
+                                       uint8_t *klist, int32_t *__restrict__ kept_index,
                                        int32_t *__restrict__ retrieve_index,
                                        int32_t *__restrict__ positions,
                                        int32_t *__restrict__ next_token,
@@ -363,30 +380,28 @@ __device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W]
     constexpr int W = GShape<G>::W;
     const int g = gl<G>();
     const int base = g * NP;
-    uint32_t km = 0;
+    const int kk = emit ? k : 0;
     if (emit) {
 #pragma unroll
         for (int r = 0; r < NP; r++) {
             const int i = base + r;
-            if (i < n && bit_w<W>(keep, i)) km |= 1u << r;
+            if (i < n && bit_w<W>(keep, i)) klist[popc_below_w<W>(keep, i)] = (uint8_t)i;
         }
-        for (int s = g; s < k; s += G)
+        for (int s = g; s < kk; s += G)
 #pragma unroll
             for (int w = 0; w < W; w++) child[s * W + w] = 0ull;
     }
     __syncwarp();
-    for (uint32_t m = km; m; m &= m - 1) {
-        const int i = base + __ffs(m) - 1;
+    for (int s = g; s < kk; s += G) {
+        const int i = klist[s];
         if (i > 0) {
-            const int s = popc_below_w<W>(keep, i);
             const int ps = popc_below_w<W>(keep, par[i]);
             atomicOr(reinterpret_cast<unsigned long long *>(&child[ps * W + (s >> 6)]), 1ull << (s & 63));
         }
     }
     __syncwarp();
-    for (uint32_t m = km; m; m &= m - 1) {
-        const int i = base + __ffs(m) - 1;
-        const int s = popc_below_w<W>(keep, i);
+    for (int s = g; s < kk; s += G) {
+        const int i = klist[s];
         uint64_t row[W];
 #pragma unroll
         for (int w = 0; w < W; w++) row[w] = 0ull;

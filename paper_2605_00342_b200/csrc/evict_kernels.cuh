@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             grp::GTree<G> t;
             grp::g_load<G>(t, tr.parent, tr.q, tr.n_nodes, b, N, active);
             float c[grp::NP];
-            grp::g_load_cost<G>(c, t, cost + (size_t)(active ? b : 0) * cost_stride);
+            grp::g_load_cost<G>(c, t, cost + (size_t)(active ? b : 0) * cost_stride, N);
             int2 *sd = reinterpret_cast<int2 *>(wscr) + gi * NMAX;
             grp::g_levels<G, true>(t, sd);
             int32_t *orow = (active && out.order) ? out.order + (size_t)b * N : nullptr;
@@ -482,10 +482,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
 #pragma unroll
             for (int w = 0; w < W; w++) keep[w] = active ? er.keep[w] : 0ull;
             uint64_t *child = reinterpret_cast<uint64_t *>(wscr) + (size_t)gi * NMAX * W;
+            uint8_t *gklist = wscr + (size_t)TPW * NMAX * W * 8 + (size_t)gi * NMAX;
             grp::g_emit<G>(keep, active ? er.n : 0, active && k > 0, k, b, N, off,
                            (active && out.pos_offset) ? __ldg(out.pos_offset + b) : 0, er.par, er.dep,
-                           child, out.kept_index, out.retrieve_index, out.positions, out.next_token,
-                           out.next_sibling, out.tree_mask);
+                           child, gklist, out.kept_index, out.retrieve_index, out.positions,
+                           out.next_token, out.next_sibling, out.tree_mask);
             __syncwarp();
         }
         tile = next;
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_select_g(evict_trees_t tr, c
     grp::GTree<G> t;
     grp::g_load<G>(t, tr.parent, tr.q, tr.n_nodes, b, N, active);
     float c[grp::NP];
-    grp::g_load_cost<G>(c, t, cost + (size_t)(active ? b : 0) * cost_stride);
+    grp::g_load_cost<G>(c, t, cost + (size_t)(active ? b : 0) * cost_stride, N);
     grp::g_levels<G, true>(t, sd_all + slot * NMAX);
     int32_t *orow = (active && order) ? order + (size_t)b * N : nullptr;
     float *prow = (active && prefix_sums) ? prefix_sums + (size_t)b * N : nullptr;

@@ -127,6 +127,66 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32])
     for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
 }
 
+// TopK of one row of BN logits under the key (logit desc, expert asc), a sorted
+// register list of KL entries (KL compile-time so the list stays in registers).
+// Entries j ≥ K hold +inf sentinels that are never displaced, so the list acts
+// as length K.  Writes the ids (if out) and ORs them into the 4-word bitset w.
+template <int KL>
+__device__ __forceinline__ uint4 topk_scan(const float *lg, int K, bool valid, int32_t *out)
+{
+    float bv[KL];
+    int bi[KL];
+    const float ninf = -__int_as_float(0x7f800000), pinf = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int j = 0; j < KL; j++) {
+        bv[j] = j < K ? ninf : pinf;
+        bi[j] = j < K ? 0x7fffffff : -1;
+    }
+    float thr = ninf;
+#pragma unroll 1
+    for (int i = 0; i < BN; i++) {
+        const float vi = lg[i];
+        if (vi > thr) {                       // later experts never beat equal logits
+            float cv = vi;
+            int ci = i;
+#pragma unroll
+            for (int j = 0; j < KL; j++) {
+                // full key (logit desc, expert asc): a displaced entry keeps its place
+                // ahead of an equal logit with a larger id
+                const bool sw = cv > bv[j] || (cv == bv[j] && ci < bi[j]);
+                const float tv = bv[j];
+                const int ti = bi[j];
+                bv[j] = sw ? cv : tv;
+                bi[j] = sw ? ci : ti;
+                cv = sw ? tv : cv;
+                ci = sw ? ti : ci;
+            }
+            // thr = bv[K-1] = the smallest of the first K (sorted) entries; a min chain
+            // (not an indexed read, which would demote the list to local memory)
+            float t = pinf;
+#pragma unroll
+            for (int j = 0; j < KL; j++) t = fminf(t, j < K ? bv[j] : pinf);
+            thr = t;
+        }
+    }
+    // scalar words (no array: the compiler would turn the word select into a
+    // dynamically indexed local-memory array)
+    uint32_t w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
+#pragma unroll
+    for (int j = 0; j < KL; j++) {
+        const int e = bi[j];
+        const bool ok = j < K && e >= 0 && e < BN;
+        const uint32_t bit = ok ? (1u << (e & 31)) : 0u;
+        const int q = e >> 5;
+        w0 |= q == 0 ? bit : 0u;
+        w1 |= q == 1 ? bit : 0u;
+        w2 |= q == 2 ? bit : 0u;
+        w3 |= q == 3 ? bit : 0u;
+        if (ok && valid && out) out[j] = e;
+    }
+    return make_uint4(w0, w1, w2, w3);
+}
+
 struct Params {
     const uint16_t *hidden;        // bf16 [L][BNrows][d]
     const int32_t *verify_offsets; // [B+1]
@@ -232,51 +292,9 @@ k_router(const __grid_constant__ CUtensorMap wmap, Params p)
             if (p.dbg_logits && valid)
                 for (int i = 0; i < 32; i++) p.dbg_logits[((size_t)l * BNrows + r) * BN + chunk * 32 + i] = v[i];
         }
-        float bv[KMAX];
-        int bi[KMAX];
-#pragma unroll
-        for (int j = 0; j < KMAX; j++) { bv[j] = -__int_as_float(0x7f800000); bi[j] = 0x7fffffff; }
-        float thr = bv[0];
-        const int K = p.K;
-#pragma unroll 1
-        for (int i = 0; i < BN; i++) {
-            const float vi = lg[i];
-            if (vi > thr) {                       // later experts never beat equal logits
-                float cv = vi;
-                int ci = i;
-#pragma unroll
-                for (int j = 0; j < KMAX; j++) {
-                    if (j < K) {
-                        // full key (logit desc, expert asc): a displaced entry
-                        // keeps its place ahead of an equal logit with a larger id
-                        const bool sw = cv > bv[j] || (cv == bv[j] && ci < bi[j]);
-                        const float tv = bv[j];
-                        const int ti = bi[j];
-                        bv[j] = sw ? cv : tv;
-                        bi[j] = sw ? ci : ti;
-                        cv = sw ? tv : cv;
-                        ci = sw ? ti : ci;
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < KMAX; j++)
-                    if (j == K - 1) thr = bv[j];
-            }
-        }
-        uint32_t w[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-        for (int j = 0; j < KMAX; j++) {
-            if (j < K && bi[j] < BN) {
-#pragma unroll
-                for (int q = 0; q < 4; q++)
-                    if ((bi[j] >> 5) == q) w[q] |= 1u << (bi[j] & 31);
-            }
-        }
-        if (valid && p.topk_ids) {
-#pragma unroll
-            for (int j = 0; j < KMAX; j++)
-                if (j < K) p.topk_ids[((size_t)l * BNrows + r) * K + j] = bi[j];
-        }
+        int32_t *tk_out = p.topk_ids ? p.topk_ids + ((size_t)l * BNrows + r) * p.K : nullptr;
+        const uint4 wq = p.K <= 8 ? topk_scan<8>(lg, p.K, valid, tk_out) : topk_scan<KMAX>(lg, p.K, valid, tk_out);
+        const uint32_t w[4] = {wq.x, wq.y, wq.z, wq.w};
         const int tree = valid ? ridx[row] / p.N : -1;
         unsigned pending = __ballot_sync(0xffffffffu, valid);
         while (pending) {
