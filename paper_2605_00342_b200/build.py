@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import glob
 import os
+import re
 import subprocess
 import sys
 from concurrent.futures import ThreadPoolExecutor
@@ -40,9 +41,40 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
+def _includes(path, seen=None):
+    """Local headers a translation unit pulls in (transitively, quoted includes only)."""
+    seen = set() if seen is None else seen
+    with open(path) as f:
+        for line in f:
+            m = re.match(r'\s*#\s*include\s+"([^"]+)"', line)
+            if not m:
+                continue
+            for d in (os.path.dirname(path), CSRC, INCLUDE):
+                h = os.path.join(d, m.group(1))
+                if os.path.exists(h) and h not in seen:
+                    seen.add(h)
+                    _includes(h, seen)
+                    break
+    return seen
+
+
+def _obj(src):
+    return os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+
+
+def _obj_stale(src):
+    obj = _obj(src)
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return any(os.path.getmtime(p) > t for p in [src, *_includes(src)])
+
+
 def _compile(src):
     os.makedirs(OBJ, exist_ok=True)
-    obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+    obj = _obj(src)
+    if not FORCE[0] and not _obj_stale(src):
+        return obj
     log = obj.replace(".o", ".ptxas.log")
     cmd = ["nvcc", *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -53,9 +85,13 @@ def _compile(src):
     return obj
 
 
+FORCE = [False]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
+    FORCE[0] = force
     srcs = sources()
     with ThreadPoolExecutor(max(1, min(len(srcs), os.cpu_count() or 4))) as ex:
         objs = list(ex.map(_compile, srcs))

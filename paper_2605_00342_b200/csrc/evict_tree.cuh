@@ -908,16 +908,37 @@ __device__ __forceinline__ void tree_union_flags(uint32_t &status, const uint8_t
         for (int j0 = 0; j0 < k; j0 += U) {
             if constexpr (IDF == 1) {
                 uint32_t v[U][R];
+                // warp-uniform fast path: a full batch of U nodes and full 32-slot rounds
+                // need no per-store guards (no divergence bookkeeping in the hot loop)
+                const bool full = (j0 + U <= k) && ((S & 31) == 0);
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int j = j0 + u;
                     const uint32_t *rowp = reinterpret_cast<const uint32_t *>(
-                        tree_u8 + (uint32_t)(j < k ? klist[j] : 0) * (uint32_t)row);
+                        tree_u8 + (uint32_t)klist[j < k ? j : 0] * (uint32_t)row);
 #pragma unroll
                     for (int c = 0; c < R; c++) {
                         const int sl = lane + 32 * c;
                         v[u][c] = (j < k && sl < S) ? __ldg(rowp + sl) : 0u;
                     }
+                }
+                if (E128 && full) {
+#pragma unroll
+                    for (int u = 0; u < U; u++)
+#pragma unroll
+                        for (int c = 0; c < R; c++) {
+                            if (32 * c >= S) continue;          // uniform: round absent
+                            uint8_t *fl = flags + c * blk + jp * 4;
+                            const uint32_t wv = v[u][c];
+                            bad |= wv & 0x80808080u;
+                            const uint32_t wm = wv & 0x7F7F7F7Fu;
+#pragma unroll
+                            for (int q = 0; q < 4; q++) {
+                                const uint32_t e = __byte_perm(wm, 0, 0x4440 | q);
+                                fl[e * 16u - (e & 3u) * 15u] = 1;
+                            }
+                        }
+                    continue;
                 }
 #pragma unroll
                 for (int u = 0; u < U; u++)

@@ -131,44 +131,86 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32])
 // register list of KL entries (KL compile-time so the list stays in registers).
 // Entries j ≥ K hold +inf sentinels that are never displaced, so the list acts
 // as length K.  Writes the ids (if out) and ORs them into the 4-word bitset w.
-template <int KL>
-__device__ __forceinline__ uint4 topk_scan(const float *lg, int K, bool valid, int32_t *out)
+__device__ __forceinline__ long long gtimer()
 {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int KL>
+__device__ __forceinline__ uint4 topk_scan(const float *lg, int K, bool valid, int32_t *out, long long *tr)
+{
+    // Candidates are visited in expert order, so a new candidate loses every tie:
+    // its rank is p = #{j < K : bv[j] >= v}; p == K never happens for a candidate
+    // (it beats the K-th entry or the list is not full).  Insertion is a branch-free shift by
+    // rank (independent selects, no dependent compare-swap chain), and a first
+    // pass bounds the work: the minimum of the 8 group maxima (16 experts each)
+    // is ≤ the 8th largest logit, so only values ≥ it can enter the list.
     float bv[KL];
     int bi[KL];
-    const float ninf = -__int_as_float(0x7f800000), pinf = __int_as_float(0x7f800000);
-#pragma unroll
-    for (int j = 0; j < KL; j++) {
-        bv[j] = j < K ? ninf : pinf;
-        bi[j] = j < K ? 0x7fffffff : -1;
-    }
-    float thr = ninf;
+    const float ninf = -__int_as_float(0x7f800000);
+    float gmin = __int_as_float(0x7f800000);
 #pragma unroll 1
-    for (int i = 0; i < BN; i++) {
-        const float vi = lg[i];
-        if (vi > thr) {                       // later experts never beat equal logits
-            float cv = vi;
-            int ci = i;
+    for (int g = 0; g < BN / 16; g++) {
+        float m = lg[g * 16];
+#pragma unroll
+        for (int i = 1; i < 16; i++) m = fmaxf(m, lg[g * 16 + i]);
+        gmin = fminf(gmin, m);
+    }
+    // valid as a lower bound for the K-th largest only when K ≤ BN/16 groups
+    // rows past T (zero-filled A tiles) have no candidates: all-equal rows would
+    // otherwise walk every element through the candidate loop
+    float thr = !valid ? __int_as_float(0x7f800000) : (K <= BN / 16) ? gmin : ninf;
+    if (tr) tr[198] = gtimer();
+    const long long c0 = tr ? clock64() : 0;
+    int nins = 0;
+#pragma unroll
+    for (int j = 0; j < KL; j++) { bv[j] = ninf; bi[j] = 0x7fffffff; }
+    int filled = 0;
+    float kth = ninf;   // current K-th entry once the list is full
+    // One warp per scheduler leaves no TLP to hide a per-element compare→branch
+    // chain, so each 32-expert chunk is screened with independent compares into a
+    // bit mask first and only the surviving candidates walk the insertion path.
+    // The state only tightens (filled, kth grow), so a screened-out value can never
+    // become a candidate again; survivors are re-checked before insertion.
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+        uint32_t cand = 0u;
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const float v = lg[c + i];
+            cand |= (v >= thr && (filled < K || v > kth)) ? (1u << i) : 0u;
+        }
+        while (cand) {
+            const int i = c + __ffs(cand) - 1;
+            cand &= cand - 1u;
+            const float vi = lg[i];
+            if (!(filled < K || vi > kth)) continue;
+            int p = 0;
+#pragma unroll
+            for (int j = 0; j < KL; j++) p += (j < K && j < filled && bv[j] >= vi) ? 1 : 0;
+            float nb[KL];
+            int ni[KL];
 #pragma unroll
             for (int j = 0; j < KL; j++) {
-                // full key (logit desc, expert asc): a displaced entry keeps its place
-                // ahead of an equal logit with a larger id
-                const bool sw = cv > bv[j] || (cv == bv[j] && ci < bi[j]);
-                const float tv = bv[j];
-                const int ti = bi[j];
-                bv[j] = sw ? cv : tv;
-                bi[j] = sw ? ci : ti;
-                cv = sw ? tv : cv;
-                ci = sw ? ti : ci;
+                const float prev = j > 0 ? bv[j - 1] : ninf;
+                const int previ = j > 0 ? bi[j - 1] : 0x7fffffff;
+                nb[j] = j < p ? bv[j] : (j == p ? vi : prev);
+                ni[j] = j < p ? bi[j] : (j == p ? i : previ);
             }
-            // thr = bv[K-1] = the smallest of the first K (sorted) entries; a min chain
-            // (not an indexed read, which would demote the list to local memory)
-            float t = pinf;
 #pragma unroll
-            for (int j = 0; j < KL; j++) t = fminf(t, j < K ? bv[j] : pinf);
-            thr = t;
+            for (int j = 0; j < KL; j++) { bv[j] = nb[j]; bi[j] = ni[j]; }
+            filled = filled < K ? filled + 1 : K;
+            nins++;
+            // sorted descending: the K-th entry is the minimum of the first K
+            // (a min-reduction, not a select, so it stays in registers)
+            kth = __int_as_float(0x7f800000);
+#pragma unroll
+            for (int j = 0; j < KL; j++) kth = fminf(kth, j < K ? bv[j] : kth);
         }
     }
+    if (tr) { tr[199] = gtimer(); tr[200] = nins; tr[201] = clock64() - c0; }
     // scalar words (no array: the compiler would turn the word select into a
     // dynamically indexed local-memory array)
     uint32_t w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
@@ -198,12 +240,6 @@ struct Params {
     long long *trace;              // [256] globaltimer trace of CTA (0,0) or null (debug only)
 };
 
-__device__ __forceinline__ long long gtimer()
-{
-    long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 
 __global__ void __launch_bounds__(THREADS, 1)
 k_router(const __grid_constant__ CUtensorMap wmap, Params p)
@@ -292,9 +328,12 @@ k_router(const __grid_constant__ CUtensorMap wmap, Params p)
             if (p.dbg_logits && valid)
                 for (int i = 0; i < 32; i++) p.dbg_logits[((size_t)l * BNrows + r) * BN + chunk * 32 + i] = v[i];
         }
+        if (tr0 && threadIdx.x == 0) p.trace[196] = gtimer();
+        long long *ttr = (tr0 && threadIdx.x == 0) ? p.trace : nullptr;
         int32_t *tk_out = p.topk_ids ? p.topk_ids + ((size_t)l * BNrows + r) * p.K : nullptr;
-        const uint4 wq = p.K <= 8 ? topk_scan<8>(lg, p.K, valid, tk_out) : topk_scan<KMAX>(lg, p.K, valid, tk_out);
+        const uint4 wq = p.K <= 8 ? topk_scan<8>(lg, p.K, valid, tk_out, ttr) : topk_scan<KMAX>(lg, p.K, valid, tk_out, ttr);
         const uint32_t w[4] = {wq.x, wq.y, wq.z, wq.w};
+        if (tr0 && threadIdx.x == 0) p.trace[197] = gtimer();
         const int tree = valid ? ridx[row] / p.N : -1;
         unsigned pending = __ballot_sync(0xffffffffu, valid);
         while (pending) {

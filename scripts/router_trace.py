@@ -13,7 +13,7 @@ uc = torch.empty((B, L), dtype=torch.int32, device="cuda"); ut = torch.empty(B, 
 ub = torch.empty((B, L, 2), dtype=torch.int64, device="cuda")
 trace = torch.zeros(256, dtype=torch.int64, device="cuda")
 f = ev.lib().evict_router_union_debug; f.argtypes = [ctypes.c_void_p] * 11; f.restype = ctypes.c_int
-for it in range(3):
+for it in range(2000):
     trace.zero_()
     rc = f(ctypes.byref(tr), ev._p(b["verify_offsets"]), ev._p(b["retrieve_index"]), ctypes.byref(rt), ev._p(uc), ev._p(ut), ev._p(ub), None, None, ev._p(trace), ev._stream())
     torch.cuda.synchronize()
@@ -22,4 +22,4 @@ print("rc", rc)
 print("mma full-wait passed (us):", [round((x - t0) / 1e3, 2) for x in t[0:32]])
 print("tma issue (us):", [round((x - t0) / 1e3, 2) for x in t[64:96]])
 print("producer stage start (us):", [round((x - t0) / 1e3, 2) for x in t[128:160]])
-print("epi start/tfull/end/sync:", [round((x - t0) / 1e3, 2) for x in t[192:196]])
+print("epi start/tfull/end/sync/staged/topk/prepass/scan:", [round((x - t0) / 1e3, 2) for x in t[192:200]], "inserts", t[200], "scan cycles", t[201])
