@@ -233,11 +233,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(evict_trees_t tr, const u
     constexpr int W = Shape<NPL>::W;
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int Epad = union_epad_u(rt.num_experts);
-    const int nrounds = (2 * rt.num_layers + 31) / 32;
-    uint8_t *flags = dsm + (size_t)warp * 16 * Epad * nrounds;
+    const int fbytes = union_flag_bytes(rt.num_layers, rt.num_experts);
+    uint8_t *flags = dsm + (size_t)warp * fbytes;
     if constexpr (IDF == 1 || IDF == 4) {
         uint4 *f4 = reinterpret_cast<uint4 *>(flags);
-        for (int i = lane; i < Epad * nrounds; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
+        for (int i = lane; i < fbytes / 16; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncwarp();
     }
     const int b = blockIdx.x * kWarps + warp;
@@ -305,7 +305,7 @@ __host__ __device__ inline int union_epad(int E) { return E <= 128 ? 128 : 256; 
 template <int G>
 __host__ __device__ inline size_t fused_scratch_bytes(int L, int E, bool flags)
 {
-    const size_t f = flags ? (size_t)16 * union_epad(E) * ((2 * L + 31) / 32) : 0;   // R rounds of 16 layers
+    const size_t f = flags ? (size_t)union_flag_bytes(L, E) : 0;
     const size_t x = fused_scratch_fixed<G>();
     return align16(f > x ? f : x);
 }
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
         if (do_union) {
             if constexpr (FLAGS) {
                 uint4 *f4 = reinterpret_cast<uint4 *>(wscr);
-                const int nz = Epad * ((2 * L + 31) / 32);   // uint4 words: R rounds × Epad·16 B
+                const int nz = union_flag_bytes(L, E) / 16;   // uint4 words
                 for (int i = lane; i < nz; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
                 __syncwarp();
             }
@@ -596,8 +596,8 @@ struct UnionLauncher {
                               cudaStream_t s)
     {
         const int blocks = (tr->batch + kWarps - 1) / kWarps;
-        const size_t dyn = (IDF == 1 || IDF == 4) ? (size_t)kWarps * 16 * union_epad_u(rt->num_experts) *
-                                                        ((2 * rt->num_layers + 31) / 32) : 0;
+        const size_t dyn = (IDF == 1 || IDF == 4) ? (size_t)kWarps * union_flag_bytes(rt->num_layers,
+                                                                                      rt->num_experts) : 0;
         auto kern = k_union<NPL, IDF, KT, EW, CL>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         kern<<<blocks, kWarps * 32, dyn, s>>>(*tr, keep, *rt, uc, ut, ub, eh, st);

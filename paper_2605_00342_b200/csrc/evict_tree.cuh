@@ -1043,6 +1043,189 @@ __device__ __forceinline__ void tree_union_flags(uint32_t &status, const uint8_t
     if (union_total && lane == 0) union_total[b] = tot;
 }
 
+// Flag bytes per warp for the top-K id union: the expert-major block below for
+// E ≤ 128 (any L ≤ 128, in passes of 64 layers), the older layer-round blocks
+// (R · 256 · 16 bytes) for E > 128.
+__host__ __device__ inline int union_flag_bytes(int L, int E)
+{
+    return E <= 128 ? 8192 : 16 * 256 * ((2 * L + 31) / 32);
+}
+
+// Top-K ids (u8 or i32, E ≤ 128) via an expert-major shared-memory flag block
+// (Eq. 5: |∪_{v kept} TopK_l(v)| per layer l).
+//
+// Slot = 2l + half (a layer's 8 ids split into two 4-id halves); lane owns
+// slots lane + 32c (round c).  Layer l lives in pass l/64, byte (l/16)%4 of
+// 32-bit word e·16 + (l%16) for expert e:
+//     flag(l, e) at byte  e·64 + 4·(l%16) + (l/16)%4
+// so a store's address is one LEA of the id (e << 6) onto a per-lane base, and
+// its bank is 16·(e&1) + l%16: lanes of different layers never collide, only
+// the two halves of one layer can.  One byte store per id (no read-modify-
+// write; duplicates idempotent).  Read-back: lane (q = lane&3, p8 = lane>>2)
+// adds 16 uint4 words bytewise (expert e = p8 + 8i, layers-words 4q..4q+3) and
+// zeroes them; an xor-shuffle over p8 leaves per-byte counts ≤ 128, i.e. the
+// union size of 16 layers per word.  Region: 8 KB per warp.
+__device__ __forceinline__ void sts_u8(uint32_t addr, uint32_t v)
+{
+    asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v));
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr)
+{
+    uint4 x;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "r"(addr));
+    return x;
+}
+__device__ __forceinline__ void sts_v4_zero(uint32_t addr)
+{
+    asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(addr), "r"(0u));
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+template <int IDF, int R, bool E128, bool BITS>
+__device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8_t *__restrict__ klist, int k,
+                                                   int b, int N, int L, int E, const void *__restrict__ ids,
+                                                   uint8_t *flags, int32_t *__restrict__ union_count,
+                                                   int32_t *__restrict__ union_total,
+                                                   uint64_t *__restrict__ union_bits)
+{
+    static_assert(IDF == 1 || IDF == 4, "flag union takes u8 or i32 ids");
+    constexpr int PASSES = (R + 3) / 4;
+    constexpr int RP = R < 4 ? R : 4;                  // rounds per pass
+    constexpr int U = IDF == 1 ? 4 : 1;                // nodes per load batch (i32 rows are 4x wider)
+    const int lane = lane_id();
+    const int S = 2 * L;
+    const uint32_t row = (uint32_t)S;                  // 4-id units per node row
+    const uint32_t fbase = (uint32_t)__cvta_generic_to_shared(flags);
+    const uint32_t lbase = fbase + 4u * (uint32_t)(lane >> 1);   // + e·64 + round byte
+    uint32_t bad = 0;
+    const bool run = status == 0;
+    int tot = 0;
+#pragma unroll 1
+    for (int pass = 0; pass < PASSES; pass++) {
+        if (run) {
+            // No store guards: a batch past k re-reads node k-1 (the union is idempotent) and
+            // a slot past 2L stores e = 0 into a layer ≥ L, whose byte is never counted
+            // (the read-back still clears it).
+            for (int j0 = 0; j0 < k; j0 += U) {
+                uint32_t v[U][RP][IDF];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int j = j0 + u;
+                    const uint32_t node = klist[j < k ? j : k - 1];
+#pragma unroll
+                    for (int cc = 0; cc < RP; cc++) {
+                        const int sl = lane + 32 * (4 * pass + cc);
+                        const bool ok = sl < S;
+                        if constexpr (IDF == 1) {
+                            const uint32_t *rp = reinterpret_cast<const uint32_t *>(ids) + ((size_t)b * N + node) * row;
+                            v[u][cc][0] = ok ? __ldg(rp + sl) : 0u;
+                        } else {
+                            const int4 *rp = reinterpret_cast<const int4 *>(ids) + ((size_t)b * N + node) * row;
+                            const int4 x = ok ? __ldg(rp + sl) : make_int4(0, 0, 0, 0);
+                            v[u][cc][0] = (uint32_t)x.x; v[u][cc][1] = (uint32_t)x.y;
+                            v[u][cc][2] = (uint32_t)x.z; v[u][cc][3] = (uint32_t)x.w;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; u++)
+#pragma unroll
+                    for (int cc = 0; cc < RP; cc++) {
+                        if constexpr (IDF == 1) {
+                            const uint32_t wv = v[u][cc][0];
+                            const uint32_t wm = wv & 0x7F7F7F7Fu;
+                            if constexpr (E128) {
+                                bad |= wv & 0x80808080u;
+                            } else {
+#pragma unroll
+                                for (int qb = 0; qb < 4; qb++) bad |= ((wv >> (8 * qb)) & 0xffu) >= (uint32_t)E;
+                            }
+#pragma unroll
+                            for (int qb = 0; qb < 4; qb++)
+                                sts_u8((__byte_perm(wm, 0, 0x4440 | qb) << 6) + (lbase + cc), 1u);
+                        } else {
+#pragma unroll
+                            for (int qb = 0; qb < 4; qb++) {
+                                const uint32_t e = v[u][cc][qb];
+                                bad |= e >= (uint32_t)E;
+                                sts_u8(((e & 127u) << 6) + (lbase + cc), 1u);
+                            }
+                        }
+                    }
+            }
+        }
+        __syncwarp();
+        if (run) {
+            if constexpr (BITS) {
+                // per-layer bit rows (test configuration only): lane = layer of this pass
+                const int EWr = (E + 63) >> 6;
+#pragma unroll 1
+                for (int li = lane; li < 64; li += 32) {
+                    const int l = 64 * pass + li;
+                    if (l >= L) break;
+                    const uint32_t fl = fbase + 4u * (uint32_t)(li & 15) + (uint32_t)(li >> 4);
+                    uint64_t lo = 0ull, hi = 0ull;
+                    for (int e = 0; e < E; e++) {
+                        const uint64_t bit = lds_u8(fl + ((uint32_t)e << 6)) ? 1ull << (e & 63) : 0ull;
+                        if (e < 64) lo |= bit; else hi |= bit;
+                    }
+                    union_bits[((size_t)b * L + l) * EWr] = lo;
+                    if (EWr > 1) union_bits[((size_t)b * L + l) * EWr + 1] = hi;
+                }
+                __syncwarp();
+            }
+            const int q = lane & 3, p8 = lane >> 2;
+            const uint32_t fw = fbase + 16u * (uint32_t)(p8 * 4 + q);
+            uint32_t a0 = 0u, a1 = 0u, a2 = 0u, a3 = 0u;
+#pragma unroll
+            for (int i = 0; i < 16; i++) {
+                const uint4 x = lds_v4(fw + 512u * i);
+                a0 += x.x; a1 += x.y; a2 += x.z; a3 += x.w;
+                sts_v4_zero(fw + 512u * i);
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                a0 += __shfl_xor_sync(kFull, a0, o);
+                a1 += __shfl_xor_sync(kFull, a1, o);
+                a2 += __shfl_xor_sync(kFull, a2, o);
+                a3 += __shfl_xor_sync(kFull, a3, o);
+            }
+            const int m = p8 & 3, bsel = p8 >> 2;
+            const uint32_t x = m == 0 ? a0 : m == 1 ? a1 : m == 2 ? a2 : a3;
+#pragma unroll
+            for (int hb = 0; hb < 2; hb++) {
+                const int byte = bsel + 2 * hb;
+                const int l = 64 * pass + 16 * byte + 4 * q + m;
+                if (l < L) {
+                    const int cnt = (int)((x >> (8 * byte)) & 0xffu);
+                    union_count[(size_t)b * L + l] = cnt;
+                    tot += cnt;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    const bool anybad = run && __any_sync(kFull, bad);
+    if (anybad) status |= EVICT_TREE_BAD_EXPERT;
+    if (!run || anybad) {
+        // a bad tree reports zero counts (and zero bit rows), like the oracle
+        for (int l = lane; l < L; l += 32) union_count[(size_t)b * L + l] = 0;
+        if constexpr (BITS) {
+            const int EWr = (E + 63) >> 6;
+            for (int i = lane; i < L * EWr; i += 32) union_bits[(size_t)b * L * EWr + i] = 0ull;
+        }
+        tot = 0;
+    }
+    __syncwarp();
+    tot = __reduce_add_sync(kFull, tot);
+    if (union_total && lane == 0) union_total[b] = tot;
+}
+
 // Dispatch: flags for top-8 ids, register OR for 1/2/4-word masks, generic otherwise.
 template <int NPL, int IDF, int KT, int EW, int R>
 __device__ __forceinline__ void tree_union(uint32_t &status, const uint8_t *__restrict__ klist, int k, int b,
@@ -1056,16 +1239,24 @@ __device__ __forceinline__ void tree_union(uint32_t &status, const uint8_t *__re
     if constexpr (IDF == 1 || IDF == 4) {
         if (expert_hist == nullptr) {   // the flag path cannot retract a bad tree's histogram rows
             const bool e128 = IDF == 1 && E == 128;
-            if (union_bits == nullptr) {
-                if (e128) tree_union_flags<NPL, IDF, R, true, false>(status, klist, k, b, N, L, E, ids, flags,
-                                                                      Epad, union_count, union_total, nullptr);
-                else tree_union_flags<NPL, IDF, R, false, false>(status, klist, k, b, N, L, E, ids, flags,
-                                                                 Epad, union_count, union_total, nullptr);
+            if (E <= 128) {
+                if (union_bits == nullptr) {
+                    if (e128) tree_union_flags64<IDF, R, true, false>(status, klist, k, b, N, L, E, ids, flags,
+                                                                      union_count, union_total, nullptr);
+                    else tree_union_flags64<IDF, R, false, false>(status, klist, k, b, N, L, E, ids, flags,
+                                                                  union_count, union_total, nullptr);
+                } else {
+                    if (e128) tree_union_flags64<IDF, R, true, true>(status, klist, k, b, N, L, E, ids, flags,
+                                                                     union_count, union_total, union_bits);
+                    else tree_union_flags64<IDF, R, false, true>(status, klist, k, b, N, L, E, ids, flags,
+                                                                 union_count, union_total, union_bits);
+                }
+            } else if (union_bits == nullptr) {
+                tree_union_flags<NPL, IDF, R, false, false>(status, klist, k, b, N, L, E, ids, flags, Epad,
+                                                            union_count, union_total, nullptr);
             } else {
-                if (e128) tree_union_flags<NPL, IDF, R, true, true>(status, klist, k, b, N, L, E, ids, flags,
-                                                                     Epad, union_count, union_total, union_bits);
-                else tree_union_flags<NPL, IDF, R, false, true>(status, klist, k, b, N, L, E, ids, flags,
-                                                                Epad, union_count, union_total, union_bits);
+                tree_union_flags<NPL, IDF, R, false, true>(status, klist, k, b, N, L, E, ids, flags, Epad,
+                                                           union_count, union_total, union_bits);
             }
         } else {
             tree_union_generic<NPL, IDF, KT, EW, (R + 1) / 2>(status, klist, k, b, N, L, K, E, idb, ids,
