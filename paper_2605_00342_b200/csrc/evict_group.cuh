@@ -96,7 +96,6 @@ struct GTree {
     int par[NP];
     float q[NP];
     float sc[NP];
-    int dep[NP];
     int n;
     uint32_t status;  // EVICT_TREE_* ; inactive groups carry BAD_SIZE
     int kstar;
@@ -174,48 +173,54 @@ __device__ __forceinline__ void g_load_cost(float (&c)[NP], GTree<G> &t, const f
 }
 
 // ------------------------------------------------------------ A2
-// sd: this group's (score bits, depth) array of NMAX entries in shared memory.
+// Score(v) = Π_{u ∈ Path(root, v)} q(u) (Eq. 7) by synchronous
+// sweeps: every sweep each node recomputes from its parent's previous score, so
+// after sweep t all depth-≤t nodes are exact with the serial root→leaf product
+// order (one fp32 rounding per edge).  The first sweep with no change ends the
+// loop: the update x(v) = q(v)·x(parent) has a unique fixed point (induction on
+// depth), so an unchanged state is the exact one — depth needs no tracking here
+// (emit recovers it from the ancestor walk).
+// sd: this group's NMAX scores in shared memory, stored swizzled: node i at
+// swz(i) = i ^ ((i >> 3) & 4), so the two 16-byte stores of the 8 lanes of a
+// quarter-warp land on 8 distinct bank groups.
+__device__ __forceinline__ int swz(int i) { return i ^ ((i >> 3) & 4); }
+
 template <int G, bool SCORES>
-__device__ __forceinline__ void g_levels(GTree<G> &t, int2 *sd)
+__device__ __forceinline__ void g_levels(GTree<G> &t, float *sd)
 {
-    const int base = gl<G>() * NP;
+    const int g = gl<G>();
+    const int base = g * NP;
     bool live[NP];
     int pidx[NP];
 #pragma unroll
     for (int r = 0; r < NP; r++) {
         const int i = base + r;
         live[r] = (t.status == 0) && (i > 0) && (i < t.n);
-        pidx[r] = live[r] ? t.par[r] : 0;
+        pidx[r] = live[r] ? swz(t.par[r]) : 0;
         t.sc[r] = 1.f;
-        t.dep[r] = 0;
-        sd[i] = make_int2(__float_as_int(1.f), 0);
     }
+    const int c0 = swz(base), c1 = swz(base + 4);
+    *reinterpret_cast<float4 *>(&sd[c0]) = make_float4(1.f, 1.f, 1.f, 1.f);
+    *reinterpret_cast<float4 *>(&sd[c1]) = make_float4(1.f, 1.f, 1.f, 1.f);
     __syncwarp();
-    while (true) {
-        bool changed = false;
-        float ns[NP];
-        int nd[NP];
+    if constexpr (SCORES) {
+        while (true) {
+            bool changed = false;
+            float ns[NP];
 #pragma unroll
-        for (int r = 0; r < NP; r++) {
-            const int2 pv = sd[pidx[r]];
-            float sv = t.sc[r];
-            if constexpr (SCORES) sv = __fmul_rn(__int_as_float(pv.x), t.q[r]);  // both ≥ +0
-            ns[r] = live[r] ? sv : t.sc[r];
-            nd[r] = live[r] ? pv.y + 1 : t.dep[r];
-            changed |= (__float_as_int(ns[r]) != __float_as_int(t.sc[r])) | (nd[r] != t.dep[r]);
+            for (int r = 0; r < NP; r++) {
+                const float sv = __fmul_rn(sd[pidx[r]], t.q[r]);   // both ≥ +0
+                ns[r] = live[r] ? sv : t.sc[r];
+                changed |= __float_as_int(ns[r]) != __float_as_int(t.sc[r]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < NP; r++) t.sc[r] = ns[r];
+            *reinterpret_cast<float4 *>(&sd[c0]) = make_float4(ns[0], ns[1], ns[2], ns[3]);
+            *reinterpret_cast<float4 *>(&sd[c1]) = make_float4(ns[4], ns[5], ns[6], ns[7]);
+            __syncwarp();
+            if (!__any_sync(kFull, changed)) break;
         }
-        __syncwarp();
-#pragma unroll
-        for (int r = 0; r < NP; r++) {
-            t.sc[r] = ns[r];
-            t.dep[r] = nd[r];
-        }
-#pragma unroll
-        for (int r = 0; r < NP; r += 2)
-            *reinterpret_cast<int4 *>(&sd[base + r]) =
-                make_int4(__float_as_int(ns[r]), nd[r], __float_as_int(ns[r + 1]), nd[r + 1]);
-        __syncwarp();
-        if (!__any_sync(kFull, changed)) break;
     }
 }
 
@@ -364,12 +369,12 @@ __device__ __forceinline__ void g_rank_argmax(GTree<G> &t, uint8_t *rk, const fl
 //   3. slot s builds its ancestor-or-self row by walking the parent chain of the
 //      shared-memory record (depth steps, no level loop), reads next-token /
 //      next-sibling from the child masks and emits the packed row.
-// par/dep: the tree's shared record arrays; child (NMAX × W words) and klist
+// par: the tree's shared parent record; child (NMAX × W words) and klist
 // (NMAX bytes): this group's scratch.
 template <int G>
 __device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W], int n, bool emit,
                                        int k, int b, int N, int off, int pos_off,
-                                       const int8_t *par, const uint8_t *dep, uint64_t *child,
+                                       const int8_t *par, uint64_t *child,
                                        uint8_t *klist, int32_t *__restrict__ kept_index,
                                        int32_t *__restrict__ retrieve_index,
                                        int32_t *__restrict__ positions,
@@ -405,7 +410,9 @@ __device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W]
         uint64_t row[W];
 #pragma unroll
         for (int w = 0; w < W; w++) row[w] = 0ull;
+        int depth = -1;
         for (int a = i; a >= 0; a = par[a]) {             // ancestor-or-self chain
+            depth++;
             const int sa = popc_below_w<W>(keep, a);
 #pragma unroll
             for (int w = 0; w < W; w++)
@@ -431,7 +438,7 @@ __device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W]
         const int rowi = off + s;
         if (kept_index) kept_index[rowi] = i;
         if (retrieve_index) retrieve_index[rowi] = b * N + i;
-        if (positions) positions[rowi] = pos_off + dep[i];
+        if (positions) positions[rowi] = pos_off + depth;   // depth = ancestor steps
         if (next_token) next_token[rowi] = nt;
         if (next_sibling) next_sibling[rowi] = ns;
         if (tree_mask) {

@@ -287,7 +287,6 @@ struct EmitRec {
     static constexpr int W = grp::GShape<G>::W;
     uint64_t keep[W];
     alignas(8) int8_t par[NMAX];
-    alignas(8) uint8_t dep[NMAX];
     int n, k;
     uint32_t status;
 };
@@ -361,7 +360,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             grp::g_load<G>(t, tr.parent, tr.q, tr.n_nodes, b, N, active);
             float c[grp::NP];
             grp::g_load_cost<G>(c, t, cost + (size_t)(active ? b : 0) * cost_stride, N);
-            int2 *sd = reinterpret_cast<int2 *>(wscr) + gi * NMAX;
+            float *sd = reinterpret_cast<float *>(wscr) + gi * NMAX;
             grp::g_levels<G, true>(t, sd);
             int32_t *orow = (active && out.order) ? out.order + (size_t)b * N : nullptr;
             float *prow = (active && out.prefix_sums) ? out.prefix_sums + (size_t)b * N : nullptr;
@@ -377,14 +376,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 if (out.keep_bits && g < WN) out.keep_bits[(size_t)b * WN + g] = t.keep[g < W ? g : 0];
                 EmitRec<G> &er = rec[slot];
                 const int base = g * grp::NP;
-                uint32_t pw[2] = {0u, 0u}, dw[2] = {0u, 0u};
+                uint32_t pw[2] = {0u, 0u};
 #pragma unroll
-                for (int r = 0; r < grp::NP; r++) {
-                    pw[r >> 2] |= (uint32_t)(t.par[r] & 0xff) << (8 * (r & 3));
-                    dw[r >> 2] |= (uint32_t)(t.dep[r] & 0xff) << (8 * (r & 3));
-                }
+                for (int r = 0; r < grp::NP; r++) pw[r >> 2] |= (uint32_t)(t.par[r] & 0xff) << (8 * (r & 3));
                 *reinterpret_cast<uint2 *>(&er.par[base]) = make_uint2(pw[0], pw[1]);
-                *reinterpret_cast<uint2 *>(&er.dep[base]) = make_uint2(dw[0], dw[1]);
                 if (g < W) er.keep[g] = t.keep[g];
                 if (g == 0) { er.n = t.n; er.k = k; er.status = t.status; }
             } else if (g == 0) {
@@ -484,7 +479,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             uint64_t *child = reinterpret_cast<uint64_t *>(wscr) + (size_t)gi * NMAX * W;
             uint8_t *gklist = wscr + (size_t)TPW * NMAX * W * 8 + (size_t)gi * NMAX;
             grp::g_emit<G>(keep, active ? er.n : 0, active && k > 0, k, b, N, off,
-                           (active && out.pos_offset) ? __ldg(out.pos_offset + b) : 0, er.par, er.dep,
+                           (active && out.pos_offset) ? __ldg(out.pos_offset + b) : 0, er.par,
                            child, gklist, out.kept_index, out.retrieve_index, out.positions,
                            out.next_token, out.next_sibling, out.tree_mask);
             __syncwarp();
@@ -508,7 +503,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_select_g(evict_trees_t tr, c
     constexpr int TPW = grp::GShape<G>::TPW;
     constexpr int NMAX = grp::GShape<G>::NMAX;
     constexpr int W = grp::GShape<G>::W;
-    __shared__ __align__(16) int2 sd_all[kSelWarps * TPW * NMAX];
+    __shared__ __align__(16) float sd_all[kSelWarps * TPW * NMAX];
     __shared__ uint8_t rk_all[kSelWarps * TPW * NMAX];
     const int warp = threadIdx.x >> 5;
     const int gi = grp::gidx<G>(), g = grp::gl<G>();

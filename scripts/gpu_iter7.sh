@@ -1,0 +1,5 @@
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
+timeout 900 python bench.py --no-extras > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; python -c "
+import json; d=json.load(open('gpurun_out/bench.json'))
+print('value', d['value'], 'kernel_ms', d['roofline']['kernel_ms'], 'frac', d['roofline']['frac'], 'step_ms', d['ms_per_step'], 'clocks', d.get('clocks'))"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 3 -c 1 -o gpurun_out/prof_fused python bench.py --steps 1 --warmup 3 --no-extras --e2e-steps 1 --cpu-seconds 1 > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log
