@@ -10,7 +10,10 @@
 //   A1 g_load            PAPER.md:48; readings Z4/Z9/Z10
 //   A2 g_levels          Eq. 7: synchronous sweeps, exact
 //                        serial root→leaf fp32 products
-//   A3–A5 g_rank_argmax  §3.2.1, Eq. 8–10
+//   A3–A5 g_rank_argmax  §3.2.1, Eq. 8–10: full
+//                        (score desc, index asc) ranking when the order row
+//                        is requested; g_select_values otherwise (value sort +
+//                        tie-aware threshold, same k*/keep bit for bit)
 //   A6 g_emit            Fig. 4(c), layout Z12
 #pragma once
 
@@ -48,6 +51,13 @@ __device__ __forceinline__ uint32_t g_max(uint32_t v)
         const uint32_t w = __shfl_xor_sync(kFull, v, o);
         v = w > v ? w : v;
     }
+    return v;
+}
+template <int G>
+__device__ __forceinline__ int g_sum(int v)
+{
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
     return v;
 }
 template <int G>
@@ -337,13 +347,13 @@ __device__ __forceinline__ void g_rank_argmax(GTree<G> &t, uint8_t *rk, const fl
         t.util = 0.f;
         t.kstar = 0;
     }
-    if (order_row != nullptr && base < N) {
+    if ((order_row != nullptr || prefix_row != nullptr) && base < N) {
 #pragma unroll
         for (int r = 0; r < NP; r++) {
             if (base + r < N) {
                 const bool v = ok && base + r < t.n;
-                order_row[base + r] = v ? node[r] : -1;
-                prefix_row[base + r] = v ? S[r] : 0.f;
+                if (order_row) order_row[base + r] = v ? node[r] : -1;
+                if (prefix_row) prefix_row[base + r] = v ? S[r] : 0.f;
             }
         }
     }
@@ -357,6 +367,148 @@ __device__ __forceinline__ void g_rank_argmax(GTree<G> &t, uint8_t *rk, const fl
         const int i = base + r;
         if (ok && i < t.n && rk[i] < t.kstar) local[i >> 6] |= 1ull << (i & 63);
     }
+#pragma unroll
+    for (int w = 0; w < W; w++) t.keep[w] = g_or64<G>(local[w]);
+}
+
+// A3–A5 without the order row: the prefix sums S[k] (Eq. 8) need only the
+// sorted score VALUES — equal scores add the same fp32 terms whichever of them
+// comes first, so S, the ratios and k* are bit-identical to the (score desc,
+// index asc) ranking.  Values sort with fmin/fmax (scores are ≥ +0, pads -1),
+// one 32-bit shuffle per cross-lane step.  The kept set is then the ranking's
+// first k* nodes: every node with score > v (v = the k*-th largest score) plus
+// the k* − #{score > v} lowest-index nodes with score == v.  prefix_row may be
+// written (values only).
+template <int G>
+__device__ __forceinline__ void g_select_values(GTree<G> &t, const float (&c)[NP], int N,
+                                                float *__restrict__ prefix_row)
+{
+    constexpr int NMAX = GShape<G>::NMAX;
+    constexpr int W = GShape<G>::W;
+    const int g = gl<G>();
+    const int base = g * NP;
+    const bool ok = t.status == 0;
+    float key[NP];
+#pragma unroll
+    for (int r = 0; r < NP; r++) key[r] = (ok && base + r < t.n) ? t.sc[r] : -1.f;
+    // bitonic sort, descending; element x = 8g + r
+#pragma unroll
+    for (int k = 2; k <= NMAX; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < NP) {
+#pragma unroll
+                for (int r = 0; r < NP; r++) {
+                    const int rp = r ^ j;
+                    if (rp > r) {
+                        const bool desc = (k < NP) ? ((r & k) != 0) : ((base & k) != 0);
+                        const float lo = fminf(key[r], key[rp]), hi = fmaxf(key[r], key[rp]);
+                        key[r] = desc ? lo : hi;
+                        key[rp] = desc ? hi : lo;
+                    }
+                }
+            } else {
+                const int lj = j / NP;
+                const bool take_hi = ((base & j) == 0) == ((base & k) == 0);
+#pragma unroll
+                for (int r = 0; r < NP; r++) {
+                    const float o = __shfl_xor_sync(kFull, key[r], lj);
+                    key[r] = take_hi ? fmaxf(key[r], o) : fminf(key[r], o);
+                }
+            }
+        }
+    }
+    // A4: S[k] = Σ_{j<k} Score(order[j])
+    float loc[NP];
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        acc = __fadd_rn(acc, key[r]);
+        loc[r] = acc;
+    }
+    float incl = acc;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+        const float v = __shfl_up_sync(kFull, incl, o, G);
+        if (g >= o) incl = __fadd_rn(incl, v);
+    }
+    float excl = __shfl_up_sync(kFull, incl, 1, G);
+    if (g == 0) excl = 0.f;
+    float S[NP];
+    uint32_t Rb[NP];
+    uint32_t best = 0;
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        S[r] = __fadd_rn(excl, loc[r]);
+        const bool v = ok && base + r < t.n;
+        const float R = v ? __fdiv_rn(S[r], c[r]) : 0.f;   // A5: IEEE division, +inf cost ⇒ 0
+        Rb[r] = v ? __float_as_uint(R) : 0u;
+        best = Rb[r] > best ? Rb[r] : best;
+    }
+    const uint32_t mx = g_max<G>(best);
+    int rfirst = NP;
+#pragma unroll
+    for (int r = NP - 1; r >= 0; r--)
+        if (ok && Rb[r] == mx && base + r < t.n) rfirst = r;
+    const unsigned has = __ballot_sync(kFull, rfirst < NP);
+    const unsigned gm = (G == 32) ? has : ((has >> (gidx<G>() * G)) & ((1u << G) - 1u));
+    const int wl = gm ? __ffs(gm) - 1 : 0;                 // smallest k wins ties (Z3)
+    const int src = (threadIdx.x & 31 & ~(G - 1)) + wl;
+    const int rf = __shfl_sync(kFull, rfirst, src);
+    float Sk = 0.f, Rk = 0.f, vk = 0.f;
+#pragma unroll
+    for (int r = 0; r < NP; r++)
+        if (r == rf) { Sk = S[r]; Rk = __uint_as_float(Rb[r]); vk = key[r]; }
+    Sk = __shfl_sync(kFull, Sk, src);
+    Rk = __shfl_sync(kFull, Rk, src);
+    vk = __shfl_sync(kFull, vk, src);
+    const int kstar = wl * NP + rf + 1;
+    if (ok) {
+        t.ehat = Sk;
+        t.util = Rk;
+        t.kstar = kstar;
+    } else {
+        t.ehat = 0.f;
+        t.util = 0.f;
+        t.kstar = 0;
+    }
+    if (prefix_row != nullptr && base < N) {
+#pragma unroll
+        for (int r = 0; r < NP; r++)
+            if (base + r < N) prefix_row[base + r] = (ok && base + r < t.n) ? S[r] : 0.f;
+    }
+    // keep: score > vk, plus the lowest-index ties (score == vk) up to k*
+    uint32_t gt = 0u, eq = 0u;
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        const bool v = ok && base + r < t.n;
+        gt |= (v && t.sc[r] > vk) ? (1u << r) : 0u;
+        eq |= (v && t.sc[r] == vk) ? (1u << r) : 0u;
+    }
+    const int ngt = g_sum<G>(__popc(gt));
+    const int neq = __popc(eq);
+    int eq_before = neq;                                   // inclusive scan over lanes
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, eq_before, o, G);
+        if (g >= o) eq_before += v;
+    }
+    eq_before -= neq;
+    int take = kstar - ngt - eq_before;                    // ties this lane may keep
+    take = take < 0 ? 0 : (take > neq ? neq : take);
+    uint32_t keq = eq;
+#pragma unroll
+    for (int r = 0; r < NP; r++) {
+        // drop the highest set bits beyond `take`
+        if (__popc(keq) > take) keq &= ~(0x80000000u >> __clz(keq));
+    }
+    const uint32_t kb = ok ? (gt | keq) : 0u;
+    uint64_t local[W];
+#pragma unroll
+    for (int w = 0; w < W; w++) local[w] = 0ull;
+#pragma unroll
+    for (int w = 0; w < W; w++)
+        if ((base >> 6) == w) local[w] = (uint64_t)kb << (base & 63);
 #pragma unroll
     for (int w = 0; w < W; w++) t.keep[w] = g_or64<G>(local[w]);
 }

@@ -364,7 +364,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             grp::g_levels<G, true>(t, sd);
             int32_t *orow = (active && out.order) ? out.order + (size_t)b * N : nullptr;
             float *prow = (active && out.prefix_sums) ? out.prefix_sums + (size_t)b * N : nullptr;
-            grp::g_rank_argmax<G>(t, rk, c, N, orow, prow);
+            if (out.order) grp::g_rank_argmax<G>(t, rk, c, N, orow, prow);   // kernel-uniform
+            else grp::g_select_values<G>(t, c, N, prow);
             const int k = t.kstar;
             if (active) {
                 if (g == 0) {
@@ -519,7 +520,8 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_select_g(evict_trees_t tr, c
     grp::g_levels<G, true>(t, sd_all + slot * NMAX);
     int32_t *orow = (active && order) ? order + (size_t)b * N : nullptr;
     float *prow = (active && prefix_sums) ? prefix_sums + (size_t)b * N : nullptr;
-    grp::g_rank_argmax<G>(t, rk_all + slot * NMAX, c, N, orow, prow);
+    if (order) grp::g_rank_argmax<G>(t, rk_all + slot * NMAX, c, N, orow, prow);   // kernel-uniform
+    else grp::g_select_values<G>(t, c, N, prow);
     if (!active) return;
     if (g == 0) {
         k_star[b] = t.kstar;

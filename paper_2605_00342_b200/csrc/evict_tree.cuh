@@ -1111,22 +1111,26 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
             // No store guards: a batch past k re-reads node k-1 (the union is idempotent) and
             // a slot past 2L stores e = 0 into a layer ≥ L, whose byte is never counted
             // (the read-back still clears it).
+            // this lane's first unit of the pass in the tree's node-row block; a node adds
+            // node·row units (32-bit: node < 128, row ≤ 256) and a round 32 units
+            const uint32_t *lane_u32 = reinterpret_cast<const uint32_t *>(ids) + (size_t)b * N * row + lane + 128 * pass;
+            const int4 *lane_i4 = reinterpret_cast<const int4 *>(ids) + (size_t)b * N * row + lane + 128 * pass;
             for (int j0 = 0; j0 < k; j0 += U) {
                 uint32_t v[U][RP][IDF];
 #pragma unroll
                 for (int u = 0; u < U; u++) {
-                    const int j = j0 + u;
-                    const uint32_t node = klist[j < k ? j : k - 1];
+                    const uint32_t node = klist[min(j0 + u, k - 1)];
 #pragma unroll
                     for (int cc = 0; cc < RP; cc++) {
-                        const int sl = lane + 32 * (4 * pass + cc);
-                        const bool ok = sl < S;
+                        const bool ok = lane + 32 * (4 * pass + cc) < S;
                         if constexpr (IDF == 1) {
-                            const uint32_t *rp = reinterpret_cast<const uint32_t *>(ids) + ((size_t)b * N + node) * row;
-                            v[u][cc][0] = ok ? __ldg(rp + sl) : 0u;
+                            const uint32_t *rp = reinterpret_cast<const uint32_t *>(
+                                reinterpret_cast<const char *>(lane_u32) + node * (4u * row));
+                            v[u][cc][0] = ok ? __ldg(rp + 32 * cc) : 0u;
                         } else {
-                            const int4 *rp = reinterpret_cast<const int4 *>(ids) + ((size_t)b * N + node) * row;
-                            const int4 x = ok ? __ldg(rp + sl) : make_int4(0, 0, 0, 0);
+                            const int4 *rp = reinterpret_cast<const int4 *>(
+                                reinterpret_cast<const char *>(lane_i4) + node * (16u * row));
+                            const int4 x = ok ? __ldg(rp + 32 * cc) : make_int4(0, 0, 0, 0);
                             v[u][cc][0] = (uint32_t)x.x; v[u][cc][1] = (uint32_t)x.y;
                             v[u][cc][2] = (uint32_t)x.z; v[u][cc][3] = (uint32_t)x.w;
                         }

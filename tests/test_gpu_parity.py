@@ -271,9 +271,10 @@ def test_union_bad_expert_and_hist(ev):
 
 
 # ------------------------------------------------------------------ fused
+@pytest.mark.parametrize("with_order", [True, False])
 @pytest.mark.parametrize("name,fmt", [("c2", "u8"), ("c4", "u8"), ("c4_60", "i32"),
                                       ("c4_60", "mask"), ("paper", "u8")])
-def test_fused_equals_oracle(ev, name, fmt):
+def test_fused_equals_oracle(ev, name, fmt, with_order):
     c = gen.CONFIGS[name]
     B = 333
     N, L, E, K = c["N"], c["L"], c["E"], c["K"]
@@ -284,9 +285,9 @@ def test_fused_equals_oracle(ev, name, fmt):
     dev_ids = T(gen.ids_to_mask(ids, E).view(np.int64)) if fmt == "mask" else T(ids)
     pos = np.full(B, 5, np.int32)
     g = npy(ev.evict_select_build_union(T(P), T(Q), T(cost), dev_ids, E, n_nodes=T(n),
-                                        pos_offset=T(pos), with_bits=True, with_order=True))
+                                        pos_offset=T(pos), with_bits=True, with_order=with_order))
     o = oracle.select(P, Q, cost, n_nodes=n, threads=8)
-    res, msgs = compare_select(o, g, n_nodes=n, check_order=True)
+    res, msgs = compare_select(o, g, n_nodes=n, check_order=with_order)
     assert not msgs, msgs[:5]
     keep = g["keep_bits"].view(np.uint64)
     ob = oracle.build_verify_tree(P, keep, n_nodes=n, pos_offset=pos)
@@ -314,8 +315,9 @@ def test_batch_stats(ev):
     assert so[4] == 1
 
 
+@pytest.mark.parametrize("with_order", [True, False])
 @pytest.mark.parametrize("N,steps", [(60, 6), (128, 8)])
-def test_select_large_batch_grouped_kernel(ev, N, steps):
+def test_select_large_batch_grouped_kernel(ev, N, steps, with_order):
     """B > 4096 takes the sub-warp (grouped) select kernel; ragged trees and a few adversarial rows."""
     B = 6000
     P, Q, n = gen.trees(91, B, N, steps, 10)
@@ -325,6 +327,36 @@ def test_select_large_batch_grouped_kernel(ev, N, steps):
     Q[8, 3] = np.nan                                      # bad prob
     C = np.tile(gen.cost_table(N), (B, 1))
     C[9::50, 2::3] = np.inf
-    g = run_select(ev, P, Q, n, C.astype(np.float32), cost_stride=N)
+    g = npy(ev.evict_select(T(P), T(Q), T(C.astype(np.float32)), n_nodes=T(n), cost_stride=N,
+                            with_order=with_order))
     o = oracle.select(P, Q, C, n_nodes=n, cost_stride=N, threads=8)
-    check_select(o, g, n)
+    res, msgs = compare_select(o, g, n_nodes=n, check_order=with_order)
+    assert not msgs, msgs[:5]
+
+
+@pytest.mark.parametrize("N", [8, 60, 64, 100, 128])
+def test_select_values_path_ties(ev, N):
+    """Without the order row the grouped kernels sort score values and rebuild the kept set from
+    the k*-th score (ties by index): tie-heavy adversarial trees, tiled past the grouped-kernel
+    threshold, must give the ranking path's k*, keep bits, ê and utility bit for bit."""
+    rng = np.random.default_rng(100 + N)
+    trees = adversarial(N, rng)
+    P, Q, n = pad_batch(trees, N)
+    reps = 4200 // len(trees) + 1
+    P, Q, n = np.tile(P, (reps, 1)), np.tile(Q, (reps, 1)), np.tile(n, reps)
+    B = len(n)
+    C = np.tile(gen.cost_table(N), (B, 1))
+    C[1::4] = 3.0                                          # constant cost: keep everything
+    C[2::4] = 0.37 * np.arange(1, N + 1)
+    C[3::4, 2::3] = np.inf
+    C = C.astype(np.float32)
+    a = npy(ev.evict_select(T(P), T(Q), T(C), n_nodes=T(n), cost_stride=N, with_order=True))
+    v = npy(ev.evict_select(T(P), T(Q), T(C), n_nodes=T(n), cost_stride=N, with_order=False))
+    for key in ("k_star", "keep_bits", "status"):
+        assert (a[key] == v[key]).all(), key
+    for key in ("e_hat", "utility"):
+        assert (a[key].view(np.uint32) == v[key].view(np.uint32)).all(), key
+    o = oracle.select(P[:len(trees)], Q[:len(trees)], C[:len(trees)], n_nodes=n[:len(trees)],
+                      cost_stride=N)
+    res, msgs = compare_select(o, {k: x[:len(trees)] for k, x in v.items()}, n_nodes=n[:len(trees)])
+    assert not msgs, msgs[:5]
