@@ -81,6 +81,7 @@ __device__ __forceinline__ uint64_t g_or64(uint64_t v)
 template <int W>
 __device__ __forceinline__ int popc_below_w(const uint64_t (&m)[W], int i)
 {
+    if constexpr (W == 1) return __popcll(m[0] & ((1ull << i) - 1ull));   // 0 ≤ i < 64 at every call
     int c = 0;
 #pragma unroll
     for (int w = 0; w < W; w++) {

@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     constexpr int PASSES = kTile / (kWarps * TPW);   // 1 (G=8) or 2 (G=16)
     constexpr bool FLAGS = IDF == 1 || IDF == 4;
     extern __shared__ __align__(16) uint8_t dsm[];
-    __shared__ int s_cnt[kTile], s_off[kTile], s_tile;
+    __shared__ int s_cnt[kTile], s_off[kTile], s_tile, s_next;
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int gi = grp::gidx<G>(), g = grp::gl<G>();
     const int N = tr.max_nodes;
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     const int Epad = union_epad(E);
     unsigned *ticket = reinterpret_cast<unsigned *>(ws);
     uint64_t *states = ws + 1;
-    if (threadIdx.x == 0) s_tile = (int)atomicAdd(ticket, 1u);
+    if (threadIdx.x == 0) { s_tile = (int)atomicAdd(ticket, 1u); s_next = 0; }
     __syncthreads();
     int tile = s_tile;
     while (tile < ntiles) {
@@ -410,11 +410,15 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 for (int i = lane; i < nz; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
                 __syncwarp();
             }
+            // trees are taken dynamically (a warp that drew small k* takes more), so the
+            // barrier after the union waits less on the unluckiest warp
 #pragma unroll 1
-            for (int it = 0; it < kTile / kWarps; it++) {
-                const int slot = (it / TPW) * (kWarps * TPW) + warp * TPW + (it % TPW);
+            while (true) {
+                int slot = 0;
+                if (lane == 0) slot = atomicAdd(&s_next, 1);
+                slot = __shfl_sync(kFull, slot, 0);
                 const int b = tile * kTile + slot;
-                if (b >= tr.batch) break;
+                if (slot >= kTile || b >= tr.batch) break;
                 EmitRec<G> &er = rec[slot];
                 const int k = er.k;
                 uint32_t st = er.status;
@@ -458,6 +462,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
         }
         __syncthreads();
         const int next = s_tile;
+        if (threadIdx.x == 0) s_next = 0;   // every warp has left this tile's union loop
         // ---------------- C: verify-tree emit, sub-warp per tree
 #pragma unroll 1
         for (int pass = 0; pass < PASSES; pass++) {
