@@ -709,6 +709,7 @@ __device__ __forceinline__ void tree_union_fast(uint32_t &status, const uint8_t 
     const int lane = lane_id();
     const int EWr = (E + 63) >> 6;
     const int P = MASK ? EWr : 2;              // parts per layer (1, 2 or 4)
+    const int lp = P == 1 ? 0 : (P == 2 ? 1 : 2);   // log2 P (shifts, not divisions)
     const int S = L * P;                       // slots
     uint32_t bs[R][NW];
 #pragma unroll
@@ -775,16 +776,20 @@ __device__ __forceinline__ void tree_union_fast(uint32_t &status, const uint8_t 
                             for (int w = 0; w < NW; w++) bs[c][w] = lb.w[w];
                         }
             } else {
+                // a batch past k re-reads node k-1 (OR is idempotent); node offsets are
+                // 32-bit byte offsets onto this lane's pointer
                 uint2 v[U][R];
+                const uint2 *lanep = reinterpret_cast<const uint2 *>(ids) + (size_t)b * N * row_elems + lane;
+                const uint32_t rowb = (uint32_t)row_elems * 8u;
 #pragma unroll
                 for (int u = 0; u < U; u++) {
-                    const int j = j0 + u;
+                    const uint32_t node = klist[min(j0 + u, k - 1)];
                     const uint2 *rowp = reinterpret_cast<const uint2 *>(
-                        (const uint64_t *)ids + ((size_t)b * N + (j < k ? klist[j] : 0)) * row_elems);
+                        reinterpret_cast<const char *>(lanep) + node * rowb);
 #pragma unroll
                     for (int c = 0; c < R; c++) {
                         const int sl = lane + 32 * c;
-                        v[u][c] = (j < k && sl < S) ? __ldg(rowp + sl) : make_uint2(0u, 0u);
+                        v[u][c] = (sl < S) ? __ldg(rowp + 32 * c) : make_uint2(0u, 0u);
                     }
                 }
 #pragma unroll
@@ -801,7 +806,7 @@ __device__ __forceinline__ void tree_union_fast(uint32_t &status, const uint8_t 
 #pragma unroll
                 for (int c = 0; c < R; c++) {
                     const int sl = lane + 32 * c;
-                    if (sl < S && (sl % P) == P - 1) {
+                    if (sl < S && (sl & (P - 1)) == P - 1) {
                         const int lo = (P - 1) * 64, rem = E - lo;
                         const uint64_t m = (uint64_t)bs[c][0] | ((uint64_t)bs[c][1] << 32);
                         if (m & ~((1ull << rem) - 1ull)) bad = 1;
@@ -816,7 +821,7 @@ __device__ __forceinline__ void tree_union_fast(uint32_t &status, const uint8_t 
 #pragma unroll
     for (int c = 0; c < R; c++) {
         const int sl = lane + 32 * c;
-        const int l = sl / P, h = sl - l * P;
+        const int l = sl >> lp, h = sl & (P - 1);
         if (zero) {
 #pragma unroll
             for (int w = 0; w < NW; w++) bs[c][w] = 0u;

@@ -89,6 +89,35 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
         : "memory");
 }
 
+__device__ __forceinline__ void cluster_sync()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_cluster(uint32_t addr, uint32_t rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float ld_cluster_f32(uint32_t addr)
+{
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+// TMA row gather (sm_100a): 4 rows × one 64-column box, written as 4 consecutive
+// 128-byte smem rows with the map's 128B swizzle.
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *map, uint32_t bar, int col, int r0,
+                                            int r1, int r2, int r3)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+        : "memory");
+}
+
 // UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart.
 __device__ __forceinline__ uint64_t umma_desc(uint32_t addr)
 {
@@ -229,11 +258,53 @@ __device__ __forceinline__ uint4 topk_scan(const float *lg, int K, bool valid, i
     return make_uint4(w0, w1, w2, w3);
 }
 
+// TopK of one row by a whole warp (sparse tiles: few valid rows would leave one
+// thread per row with no latency hiding).  Lane holds experts lane + 32q; each of
+// the K rounds takes the warp max under (logit desc, expert asc) with two
+// reductions (orderable logit bits, then the smallest expert among the maxima)
+// and retires the winner.  Every lane ends with the same ids and bit words.
+__device__ __forceinline__ uint32_t f2ord(float f)
+{
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ uint4 topk_warp_row(const float *lgrow, int K, int32_t *out, int lane)
+{
+    float v[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) v[q] = lgrow[lane + 32 * q];
+    uint32_t w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
+    const float ninf = -__int_as_float(0x7f800000);
+#pragma unroll 1
+    for (int j = 0; j < K; j++) {
+        const float m = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+        const uint32_t u = f2ord(m);
+        const uint32_t U = __reduce_max_sync(0xffffffffu, u);
+        int el = 255;
+#pragma unroll
+        for (int q = 3; q >= 0; q--) el = (v[q] == m) ? lane + 32 * q : el;
+        const int e = (int)__reduce_min_sync(0xffffffffu, u == U ? (uint32_t)el : 255u);
+        if ((e & 31) == lane) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) v[q] = (q == (e >> 5)) ? ninf : v[q];
+        }
+        const uint32_t bit = 1u << (e & 31);
+        const int qw = e >> 5;
+        w0 |= qw == 0 ? bit : 0u;
+        w1 |= qw == 1 ? bit : 0u;
+        w2 |= qw == 2 ? bit : 0u;
+        w3 |= qw == 3 ? bit : 0u;
+        if (out && lane == 0) out[j] = e;
+    }
+    return make_uint4(w0, w1, w2, w3);
+}
+
 struct Params {
     const uint16_t *hidden;        // bf16 [L][BNrows][d]
     const int32_t *verify_offsets; // [B+1]
     const int32_t *retrieve_index; // [cap]
     int L, B, N, d, K;
+    int splits;                    // k-splits = cluster size along z (1: no cluster)
     unsigned long long *bits;      // [B][L][2]
     int32_t *topk_ids;             // [L][B*N][K] or null
     float *dbg_logits;             // [L][B*N][128] or null (debug entry point only)
@@ -242,7 +313,7 @@ struct Params {
 
 
 __global__ void __launch_bounds__(THREADS, 1)
-k_router(const __grid_constant__ CUtensorMap wmap, Params p)
+k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap hmap, Params p)
 {
     extern __shared__ uint8_t smem_raw[];
     const int T = __ldg(p.verify_offsets + p.B);
@@ -261,10 +332,14 @@ k_router(const __grid_constant__ CUtensorMap wmap, Params p)
     auto Bs = [&](int s) { return base_u32 + s * STAGE_BYTES + A_BYTES; };
 
     const bool tr0 = p.trace && blockIdx.x == 0 && blockIdx.y == 0;
+    const int nrow = T - m0 < BM ? T - m0 : BM;   // valid rows of this tile
+    // sparse tiles gather their few hidden rows with TMA (gather4, one issuing thread);
+    // dense tiles use 128 cp.async producers (one TMA thread would serialise 32 gathers)
+    const bool sparse = nrow <= 32;
     if (tr0 && threadIdx.x == 0) p.trace[250] = gtimer();
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(full0 + 8 * s, NPROD + 1);
+            mbar_init(full0 + 8 * s, sparse ? 1 : NPROD + 1);
             mbar_init(empty0 + 8 * s, 1);
         }
         mbar_init(tfull, 1);
@@ -283,52 +358,145 @@ k_router(const __grid_constant__ CUtensorMap wmap, Params p)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     const int KB = p.d / BK;
+    // split z of S takes k-blocks [kb0, kb1); the S CTAs of a cluster share (tile, layer)
+    const int S = p.splits, z = blockIdx.z;
+    const int kb0 = (int)(((long)KB * z) / S), kb1 = (int)(((long)KB * (z + 1)) / S);
+    const int NKB = kb1 - kb0;
     const size_t BNrows = (size_t)p.B * p.N;
+    const int row = warp * 32 + lane;         // epilogue row (warps 0–3)
+    float *lg = reinterpret_cast<float *>(base) + (size_t)(row & (BM - 1)) * (BN + 1);
 
     if (warp < 4) {
-        // ---- producers: gather 128 rows × 64 bf16 per stage, swizzled
-        const int t = threadIdx.x, c = t & 7, r0 = t >> 3;
-        const uint16_t *hl = p.hidden + (size_t)l * BNrows * p.d;
-        for (int kb = 0; kb < KB; kb++) {
-            const int s = kb % STAGES;
-            if (kb >= STAGES) mbar_wait(empty0 + 8 * s, ((kb / STAGES) - 1) & 1);
-            if (tr0 && threadIdx.x == 0 && kb < 64) p.trace[128 + kb] = gtimer();
+        if (!sparse) {
+            // ---- producers: gather 128 rows × 64 bf16 per stage, 128-byte XOR swizzle
+            const int t = threadIdx.x, c = t & 7, r0 = t >> 3;
+            const uint16_t *hl = p.hidden + (size_t)l * BNrows * p.d;
+            for (int i = 0; i < NKB; i++) {
+                const int kb = kb0 + i, s = i % STAGES;
+                if (i >= STAGES) mbar_wait(empty0 + 8 * s, ((i / STAGES) - 1) & 1);
+                if (tr0 && threadIdx.x == 0 && i < 64) p.trace[128 + i] = gtimer();
 #pragma unroll
-            for (int j = 0; j < 8; j++) {
-                const int row = r0 + 16 * j;
-                const int rid = ridx[row];
-                const uint16_t *src = hl + (size_t)(rid < 0 ? 0 : rid) * p.d + kb * BK + c * 8;
-                cp_async16(A(s) + row * 128 + ((c ^ (row & 7)) << 4), src, rid < 0 ? 0u : 16u);
+                for (int j = 0; j < 8; j++) {
+                    const int rr = r0 + 16 * j;
+                    const int rid = ridx[rr];
+                    const uint16_t *src = hl + (size_t)(rid < 0 ? 0 : rid) * p.d + kb * BK + c * 8;
+                    cp_async16(A(s) + rr * 128 + ((c ^ (rr & 7)) << 4), src, rid < 0 ? 0u : 16u);
+                }
+                // arrive on full[s] asynchronously once this thread's copies have landed:
+                // the producer never blocks on its own loads, only on slot reuse (empty[s])
+                cp_async_arrive_noinc(full0 + 8 * s);
             }
-            // arrive on full[s] asynchronously once this thread's copies have landed:
-            // the producer never blocks on its own loads, only on slot reuse (empty[s])
-            cp_async_arrive_noinc(full0 + 8 * s);
+            cp_async_wait<0>();
         }
-        cp_async_wait<0>();
-
-        // ---- epilogue: TMEM → registers → TopK → union bits
+        // ---- stage the (partial) accumulator: TMEM → registers → shared memory
         if (tr0 && threadIdx.x == 0) p.trace[192] = gtimer();
         mbar_wait(tfull, 0);
         if (tr0 && threadIdx.x == 0) p.trace[193] = gtimer();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int row = warp * 32 + lane;
-        const int r = m0 + row;
-        const bool valid = r < T;
-        // stage the row's 128 logits in shared memory (the operand ring is free now;
-        // stride 129 floats: thread t's element i sits in bank (t + i) % 32), then run a
-        // compact, non-unrolled TopK scan over them (a fully unrolled register scan
-        // overflows the instruction cache)
-        float *lg = reinterpret_cast<float *>(base) + (size_t)row * (BN + 1);
+        // the operand ring is free now; stride 129 floats: thread t's element i sits in
+        // bank (t + i) % 32
 #pragma unroll 1
         for (int chunk = 0; chunk < BN / 32; chunk++) {
             float v[32];
             tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + chunk * 32, v);
 #pragma unroll
             for (int i = 0; i < 32; i++) lg[chunk * 32 + i] = v[i];
-            if (p.dbg_logits && valid)
-                for (int i = 0; i < 32; i++) p.dbg_logits[((size_t)l * BNrows + r) * BN + chunk * 32 + i] = v[i];
         }
         if (tr0 && threadIdx.x == 0) p.trace[196] = gtimer();
+    } else if (warp == 4) {
+        // ---- MMA issuer
+        if (lane == 0) {
+            for (int i = 0; i < NKB; i++) {
+                const int s = i % STAGES;
+                mbar_wait(full0 + 8 * s, (i / STAGES) & 1);
+                if (tr0 && i < 64) p.trace[i] = gtimer();
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                for (int k = 0; k < BK / 16; k++)
+                    umma_bf16(tmem, umma_desc(A(s) + 32 * k), umma_desc(Bs(s) + 32 * k), (i | k) != 0);
+                umma_commit(empty0 + 8 * s);
+            }
+            umma_commit(tfull);
+        }
+        __syncwarp();
+    } else {
+        // ---- operands via TMA: W_g k-block (2D tile) + the tile's hidden rows (gather4,
+        // only the groups holding valid rows; rows past T in the last group repeat a valid
+        // row — an A row only feeds its own D row, which nobody reads)
+        if (lane == 0) {
+            const int ng = sparse ? (nrow + 3) >> 2 : 0;
+            const int lrow = l * (int)BNrows;
+            for (int i = 0; i < NKB; i++) {
+                const int kb = kb0 + i, s = i % STAGES;
+                if (i >= STAGES) mbar_wait(empty0 + 8 * s, ((i / STAGES) - 1) & 1);
+                if (tr0 && i < 64) p.trace[64 + i] = gtimer();
+                mbar_arrive_tx(full0 + 8 * s, B_BYTES + 512u * ng);
+                tma_load_2d(Bs(s), &wmap, full0 + 8 * s, kb * BK, l * BN);
+                for (int g4 = 0; g4 < ng; g4++) {
+                    int rr[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int row_ = 4 * g4 + u;
+                        rr[u] = lrow + ridx[row_ < nrow ? row_ : 0];
+                    }
+                    tma_gather4(A(s) + g4 * 512, &hmap, full0 + 8 * s, kb * BK, rr[0], rr[1], rr[2], rr[3]);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (tr0 && threadIdx.x == 0) p.trace[194] = gtimer();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tr0 && threadIdx.x == 0) p.trace[195] = gtimer();
+    if (warp == 4) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+    }
+    if (S > 1) cluster_sync();                // every split's partial is staged
+
+    if (z == 0 && warp < 4) {
+        // ---- leader: ordered sum of the partials (split 0 + 1 + … : deterministic), TopK, union
+        const int r = m0 + row;
+        const bool valid = r < T;
+        if (S > 1) {
+            // the valid rows' partials are one contiguous block: 128 threads stream it
+            // coalesced from each remote split (independent loads, 4 in flight per thread)
+            const int nf = nrow * (BN + 1);
+            float *lgf = reinterpret_cast<float *>(base);
+            const uint32_t mine = smem_u32(base);
+#pragma unroll 1
+            for (int zz = 1; zz < S; zz++) {
+                const uint32_t rem = mapa_cluster(mine, (uint32_t)zz);
+                int f = threadIdx.x;
+#pragma unroll 1
+                for (; f + 3 * BM < nf; f += 4 * BM) {
+                    const float a0 = ld_cluster_f32(rem + 4u * f), a1 = ld_cluster_f32(rem + 4u * (f + BM));
+                    const float a2 = ld_cluster_f32(rem + 4u * (f + 2 * BM)), a3 = ld_cluster_f32(rem + 4u * (f + 3 * BM));
+                    lgf[f] += a0; lgf[f + BM] += a1; lgf[f + 2 * BM] += a2; lgf[f + 3 * BM] += a3;
+                }
+                for (; f < nf; f += BM) lgf[f] += ld_cluster_f32(rem + 4u * f);
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");   // warps 0–3 only
+        }
+        if (p.dbg_logits && valid)
+            for (int i = 0; i < BN; i++) p.dbg_logits[((size_t)l * BNrows + r) * BN + i] = lg[i];
+        if (nrow <= 32) {
+            // sparse tile: a warp per row (rows warp, warp + 4, …), one atomic pair per row
+#pragma unroll 1
+            for (int rr = warp; rr < nrow; rr += 4) {
+                const int rg = m0 + rr;
+                int32_t *o = p.topk_ids ? p.topk_ids + ((size_t)l * BNrows + rg) * p.K : nullptr;
+                const float *lrow = reinterpret_cast<const float *>(base) + (size_t)rr * (BN + 1);
+                const uint4 wr = topk_warp_row(lrow, p.K, o, lane);
+                if (lane == 0) {
+                    unsigned long long *dst = p.bits + ((size_t)(ridx[rr] / p.N) * p.L + l) * 2;
+                    atomicOr(dst, (unsigned long long)wr.x | ((unsigned long long)wr.y << 32));
+                    atomicOr(dst + 1, (unsigned long long)wr.z | ((unsigned long long)wr.w << 32));
+                }
+            }
+            if (tr0 && threadIdx.x == 0) p.trace[197] = gtimer();
+        } else {
         long long *ttr = (tr0 && threadIdx.x == 0) ? p.trace : nullptr;
         int32_t *tk_out = p.topk_ids ? p.topk_ids + ((size_t)l * BNrows + r) * p.K : nullptr;
         const uint4 wq = p.K <= 8 ? topk_scan<8>(lg, p.K, valid, tk_out, ttr) : topk_scan<KMAX>(lg, p.K, valid, tk_out, ttr);
@@ -351,43 +519,9 @@ k_router(const __grid_constant__ CUtensorMap wmap, Params p)
             }
             pending &= ~grp;
         }
-    } else if (warp == 4) {
-        // ---- MMA issuer
-        if (lane == 0) {
-            for (int kb = 0; kb < KB; kb++) {
-                const int s = kb % STAGES;
-                mbar_wait(full0 + 8 * s, (kb / STAGES) & 1);
-                if (tr0 && kb < 64) p.trace[kb] = gtimer();
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-                for (int k = 0; k < BK / 16; k++)
-                    umma_bf16(tmem, umma_desc(A(s) + 32 * k), umma_desc(Bs(s) + 32 * k), (kb | k) != 0);
-                umma_commit(empty0 + 8 * s);
-            }
-            umma_commit(tfull);
         }
-        __syncwarp();
-    } else {
-        // ---- W_g k-blocks via TMA
-        if (lane == 0) {
-            for (int kb = 0; kb < KB; kb++) {
-                const int s = kb % STAGES;
-                if (kb >= STAGES) mbar_wait(empty0 + 8 * s, ((kb / STAGES) - 1) & 1);
-                if (tr0 && kb < 64) p.trace[64 + kb] = gtimer();
-                mbar_arrive_tx(full0 + 8 * s, B_BYTES);
-                tma_load_2d(Bs(s), &wmap, full0 + 8 * s, kb * BK, l * BN);
-            }
-        }
-        __syncwarp();
     }
-    if (tr0 && threadIdx.x == 0) p.trace[194] = gtimer();
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (tr0 && threadIdx.x == 0) p.trace[195] = gtimer();
-    if (warp == 4) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
-    }
+    if (S > 1) cluster_sync();                // partials stay alive until the leader has read them
 }
 
 __global__ void k_finalize(int B, int L, const unsigned long long *bits, int32_t *count, int32_t *total)
@@ -482,6 +616,15 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return EVICT_ERR_INVALID_ARG;
+    // hidden rows are gathered by TMA with int32 row coordinates over the [L·B·N][d] view
+    if ((size_t)L * B * N >= (size_t)1 << 31) return EVICT_ERR_UNSUPPORTED;
+    CUtensorMap hmap;
+    cuuint64_t hdims[2] = {(cuuint64_t)d, (cuuint64_t)L * B * N};
+    cuuint32_t hbox[2] = {BK, 1};
+    if (enc(&hmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(rt->hidden), hdims, strides, hbox, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return EVICT_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     static std::once_flag attr_once;
     std::call_once(attr_once, [] { cudaFuncSetAttribute(k_router, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES); });
@@ -495,8 +638,61 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     p.topk_ids = topk_ids;
     p.dbg_logits = dbg_logits;
     p.trace = trace;
-    dim3 grid((unsigned)(((size_t)B * N + BM - 1) / BM), (unsigned)L);
-    k_router<<<grid, THREADS, SMEM_BYTES, s>>>(map, p);
+    // Split the d-reduction over a cluster of S CTAs when the (tile, layer) grid would leave
+    // SMs idle (batch-1 serving: one 128-row tile × L layers < #SMs).  The host bounds the
+    // active tiles by B·N rows (T is device-resident).
+    const int tiles = (int)(((size_t)B * N + BM - 1) / BM);
+    const int KB = d / BK;
+    int S = evict::dev_sms() / (tiles * L);
+    S = S < 1 ? 1 : (S > 4 ? 4 : S);
+    if (S > KB) S = KB;
+    // clusters are placed GPC by GPC: take the largest S whose tiles·L clusters are all
+    // co-resident (a second wave would double the time)
+    static int max_clusters[5] = {-1, -1, -1, -1, -1};
+    static std::mutex mc_mu;
+    while (S > 1) {
+        int mc;
+        {
+            std::lock_guard<std::mutex> g(mc_mu);
+            if (max_clusters[S] < 0) {
+                cudaLaunchConfig_t q = {};
+                q.gridDim = dim3((unsigned)S, 1u, 1u);
+                q.blockDim = dim3(THREADS, 1, 1);
+                q.dynamicSmemBytes = SMEM_BYTES;
+                cudaLaunchAttribute a[1];
+                a[0].id = cudaLaunchAttributeClusterDimension;
+                a[0].val.clusterDim.x = (unsigned)S;
+                a[0].val.clusterDim.y = 1;
+                a[0].val.clusterDim.z = 1;
+                q.attrs = a;
+                q.numAttrs = 1;
+                int n = 0;
+                max_clusters[S] = cudaOccupancyMaxActiveClusters(&n, k_router, &q) == cudaSuccess ? n : 0;
+            }
+            mc = max_clusters[S];
+        }
+        if (mc >= tiles * L) break;
+        S--;
+    }
+    p.splits = S;
+    if (S == 1) {
+        dim3 grid((unsigned)tiles, (unsigned)L, 1u);
+        k_router<<<grid, THREADS, SMEM_BYTES, s>>>(map, hmap, p);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)tiles, (unsigned)L, (unsigned)S);
+        cfg.blockDim = dim3(THREADS, 1, 1);
+        cfg.dynamicSmemBytes = SMEM_BYTES;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = (unsigned)S;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, k_router, map, hmap, p) != cudaSuccess) return EVICT_ERR_CUDA;
+    }
     if (cudaGetLastError() != cudaSuccess) return EVICT_ERR_CUDA;
     k_finalize<<<(B + 7) / 8, 256, 0, s>>>(B, L, reinterpret_cast<const unsigned long long *>(union_bits),
                                            union_count, union_total);
