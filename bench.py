@@ -316,7 +316,7 @@ def router_bench(ev, gen, torch, stream):
         h = gen.hidden_cuda(11, B, Nn, L, d, mode=1)
         w = gen.wgate_cuda(12, L, N_EXPERTS, d, mode=1, scale_log2=-5)
         T = int(b["verify_offsets"][-1])
-        rc = ev.RouterCall(b["verify_offsets"], b["retrieve_index"], h, w, TOP_K, B, Nn)
+        rc = ev.RouterCall(b["verify_offsets"], b["retrieve_index"], h, w, TOP_K, B, Nn, max_rows=T)
         for _ in range(3):
             rc(stream)
         reps = 50

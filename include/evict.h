@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define EVICT_ABI_VERSION 1
+#define EVICT_ABI_VERSION 2
 #define EVICT_MAX_NODES 128   /* N ≤ 128 ⇒ W ≤ 2 mask words */
 #define EVICT_MAX_EXPERTS 256 /* Ling-flash-2.0 has 256 experts */
 #define EVICT_MAX_TOPK 16
@@ -211,7 +211,12 @@ evict_status_t evict_select_build_union(const evict_trees_t *trees, const float 
  *   hidden  bf16 [L][B*N][d]  per-layer hidden states of every draft node
  *   w_gate  bf16 [L][E][d]    router weights, rows = expert centroids
  *   topk_ids int32 [L][B*N][K] (or NULL): per packed row r, at [l][r][j]
- * Supported: E = 128, d % 64 == 0, K ≤ 16.
+ *   max_rows: an upper bound on T = verify_offsets[B] known to the caller
+ *            (e.g. its verify-token budget), or 0 for B·N.  It sizes the
+ *            launch only (grid, k-split, ring depth).  Contract: T ≤
+ *            max_rows (T is device-resident, so the host cannot check it;
+ *            rows at or past ceil(max_rows/128)·128 would not be routed).
+ * Supported: E = 128, d % 64 == 0, K ≤ 16, L·B·N < 2^31.
  * ------------------------------------------------------------------------- */
 typedef struct {
     int32_t num_layers;
@@ -220,6 +225,7 @@ typedef struct {
     int32_t hidden_dim;  /* d */
     const void *hidden;  /* bf16 [L][B*N][d] */
     const void *w_gate;  /* bf16 [L][E][d] */
+    int32_t max_rows;    /* upper bound on T, or 0 (= B*N); launch sizing only */
 } evict_router_t;
 
 evict_status_t evict_router_union(const evict_trees_t *trees, const int32_t *verify_offsets,

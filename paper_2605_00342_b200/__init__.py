@@ -47,7 +47,7 @@ class _Routing(ctypes.Structure):
 class _Router(ctypes.Structure):
     _fields_ = [("num_layers", ctypes.c_int32), ("num_experts", ctypes.c_int32),
                 ("top_k", ctypes.c_int32), ("hidden_dim", ctypes.c_int32),
-                ("hidden", ctypes.c_void_p), ("w_gate", ctypes.c_void_p)]
+                ("hidden", ctypes.c_void_p), ("w_gate", ctypes.c_void_p), ("max_rows", ctypes.c_int32)]
 
 
 _OUT_FIELDS = ["k_star", "e_hat", "utility", "keep_bits", "order", "prefix_sums", "pos_offset",
@@ -293,7 +293,7 @@ class FusedCall:
 
 # ----------------------------------------------------------------- router (A8 → A7)
 def evict_router_union(verify_offsets, retrieve_index, hidden, w_gate, top_k, batch, max_nodes,
-                       with_topk=False, stream=None):
+                       with_topk=False, max_rows=0, stream=None):
     """hidden: bf16 [L][B*N][d]; w_gate: bf16 [L][E][d]; rows from evict_build_verify_tree."""
     L, BN, d = hidden.shape
     E = w_gate.shape[1]
@@ -305,7 +305,7 @@ def evict_router_union(verify_offsets, retrieve_index, hidden, w_gate, top_k, ba
     if with_topk:
         out["topk_ids"] = torch.full((L, BN, top_k), -1, dtype=torch.int32, device=dev)
     tr = _Trees(batch, max_nodes, None, None, None)
-    rt = _Router(L, E, top_k, d, _p(hidden), _p(w_gate))
+    rt = _Router(L, E, top_k, d, _p(hidden), _p(w_gate), int(max_rows))
     rc = lib().evict_router_union(ctypes.byref(tr), _p(verify_offsets), _p(retrieve_index),
                                   ctypes.byref(rt), _p(out["union_count"]), _p(out["union_total"]),
                                   _p(out["union_bits"]), _p(out.get("topk_ids")), _stream(stream))
@@ -317,7 +317,7 @@ class RouterCall:
     """A pre-marshalled evict_router_union call with pre-allocated outputs (timing loops, graphs)."""
 
     def __init__(self, verify_offsets, retrieve_index, hidden, w_gate, top_k, batch, max_nodes,
-                 with_topk=False):
+                 with_topk=False, max_rows=0):
         L, BN, d = hidden.shape
         E = w_gate.shape[1]
         dev = hidden.device
@@ -329,7 +329,7 @@ class RouterCall:
         if with_topk:
             self.t["topk_ids"] = torch.full((L, BN, top_k), -1, dtype=torch.int32, device=dev)
         self.tr = _Trees(batch, max_nodes, None, None, None)
-        self.rt = _Router(L, E, top_k, d, _p(hidden), _p(w_gate))
+        self.rt = _Router(L, E, top_k, d, _p(hidden), _p(w_gate), int(max_rows))
         self.args = (_p(verify_offsets), _p(retrieve_index))
         self.fn = lib().evict_router_union
 

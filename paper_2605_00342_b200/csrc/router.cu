@@ -27,14 +27,18 @@ namespace evict {
 namespace router {
 
 constexpr int BM = 128, BN = 128, BK = 64;
-constexpr int STAGES = 6;
+// operand ring depth (template): 6 stages (1 CTA/SM) when the grid fits one wave,
+// 3 stages (2 CTAs/SM, 256 of 512 TMEM columns) when tiles × layers exceed the SMs
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_BYTES = BN * BK * 2;  // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int THREADS = 192;
 constexpr int NPROD = 128;
 constexpr int KMAX = 16;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, ridx*/ + 512;
+__host__ __device__ constexpr int smem_bytes(int stages)
+{
+    return stages * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, ridx*/ + 512;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -312,7 +316,8 @@ struct Params {
 };
 
 
-__global__ void __launch_bounds__(THREADS, 1)
+template <int STAGES>
+__global__ void __launch_bounds__(THREADS, STAGES <= 3 ? 2 : 1)
 k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap hmap, Params p)
 {
     extern __shared__ uint8_t smem_raw[];
@@ -627,7 +632,10 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
         return EVICT_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     static std::once_flag attr_once;
-    std::call_once(attr_once, [] { cudaFuncSetAttribute(k_router, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES); });
+    std::call_once(attr_once, [] {
+        cudaFuncSetAttribute(k_router<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(6));
+        cudaFuncSetAttribute(k_router<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(3));
+    });
     if (cudaMemsetAsync(union_bits, 0, sizeof(uint64_t) * (size_t)B * L * 2, s) != cudaSuccess) return EVICT_ERR_CUDA;
     Params p;
     p.hidden = (const uint16_t *)rt->hidden;
@@ -641,7 +649,10 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     // Split the d-reduction over a cluster of S CTAs when the (tile, layer) grid would leave
     // SMs idle (batch-1 serving: one 128-row tile × L layers < #SMs).  The host bounds the
     // active tiles by B·N rows (T is device-resident).
-    const int tiles = (int)(((size_t)B * N + BM - 1) / BM);
+    if (rt->max_rows < 0) return EVICT_ERR_INVALID_ARG;
+    const size_t rows_bound = rt->max_rows > 0 && (size_t)rt->max_rows < (size_t)B * N ? (size_t)rt->max_rows
+                                                                                          : (size_t)B * N;
+    const int tiles = (int)((rows_bound + BM - 1) / BM);
     const int KB = d / BK;
     int S = evict::dev_sms() / (tiles * L);
     S = S < 1 ? 1 : (S > 4 ? 4 : S);
@@ -658,7 +669,7 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
                 cudaLaunchConfig_t q = {};
                 q.gridDim = dim3((unsigned)S, 1u, 1u);
                 q.blockDim = dim3(THREADS, 1, 1);
-                q.dynamicSmemBytes = SMEM_BYTES;
+                q.dynamicSmemBytes = smem_bytes(6);
                 cudaLaunchAttribute a[1];
                 a[0].id = cudaLaunchAttributeClusterDimension;
                 a[0].val.clusterDim.x = (unsigned)S;
@@ -667,7 +678,7 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
                 q.attrs = a;
                 q.numAttrs = 1;
                 int n = 0;
-                max_clusters[S] = cudaOccupancyMaxActiveClusters(&n, k_router, &q) == cudaSuccess ? n : 0;
+                max_clusters[S] = cudaOccupancyMaxActiveClusters(&n, k_router<6>, &q) == cudaSuccess ? n : 0;
             }
             mc = max_clusters[S];
         }
@@ -677,12 +688,13 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     p.splits = S;
     if (S == 1) {
         dim3 grid((unsigned)tiles, (unsigned)L, 1u);
-        k_router<<<grid, THREADS, SMEM_BYTES, s>>>(map, hmap, p);
+        if ((long)tiles * L > evict::dev_sms()) k_router<3><<<grid, THREADS, smem_bytes(3), s>>>(map, hmap, p);
+        else k_router<6><<<grid, THREADS, smem_bytes(6), s>>>(map, hmap, p);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)tiles, (unsigned)L, (unsigned)S);
         cfg.blockDim = dim3(THREADS, 1, 1);
-        cfg.dynamicSmemBytes = SMEM_BYTES;
+        cfg.dynamicSmemBytes = smem_bytes(6);
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -691,7 +703,7 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
         attr[0].val.clusterDim.z = (unsigned)S;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, k_router, map, hmap, p) != cudaSuccess) return EVICT_ERR_CUDA;
+        if (cudaLaunchKernelEx(&cfg, k_router<6>, map, hmap, p) != cudaSuccess) return EVICT_ERR_CUDA;
     }
     if (cudaGetLastError() != cudaSuccess) return EVICT_ERR_CUDA;
     k_finalize<<<(B + 7) / 8, 256, 0, s>>>(B, L, reinterpret_cast<const unsigned long long *>(union_bits),

@@ -29,7 +29,7 @@ import ctypes
 lg = torch.zeros((L, B * N, 128), dtype=torch.float32, device="cuda")
 tr = ev._Trees(B, N, None, None, None)
 hh = cu(h.view(np.int16)).view(torch.bfloat16); ww = cu(w.view(np.int16)).view(torch.bfloat16)
-rt = ev._Router(L, E, K, d, ev._p(hh), ev._p(ww))
+rt = ev._Router(L, E, K, d, ev._p(hh), ev._p(ww), 0)
 uc = torch.empty((B, L), dtype=torch.int32, device="cuda"); ut = torch.empty(B, dtype=torch.int32, device="cuda")
 ub = torch.empty((B, L, 2), dtype=torch.int64, device="cuda"); tk2 = torch.empty((L, B * N, K), dtype=torch.int32, device="cuda")
 lib = ev.lib(); f = lib.evict_router_union_debug; f.argtypes = [ctypes.c_void_p] * 10; f.restype = ctypes.c_int

@@ -41,15 +41,17 @@ def kept_rows(ev, B, N, steps, topk, seed):
     (5, 32, 4, 8, 3, 64, 2),          # small d, K=2
     (3, 8, 3, 2, 2, 128, 16),         # K = 16
 ])
-def test_router_integer_inputs_bit_exact(ev, B, N, steps, topk, L, d, K):
+@pytest.mark.parametrize("hint", [False, True])
+def test_router_integer_inputs_bit_exact(ev, B, N, steps, topk, L, d, K, hint):
     """Integer-valued bf16 h, W_g ⇒ every fp32 partial sum is exact ⇒ TopK (with the
     (logit desc, expert asc) tie rule) must match the fp64 oracle bit for bit."""
     E = 128
     P, n, sel, b = kept_rows(ev, B, N, steps, topk, seed=21)
     h = gen.hidden(31, B, N, L, d, mode=0)
     w = gen.wgate(32, L, E, d, mode=0)
+    T = int(b["verify_offsets"][-1])
     g = ev.evict_router_union(b["verify_offsets"], b["retrieve_index"], bf16(h), bf16(w), K, B, N,
-                              with_topk=True)
+                              with_topk=True, max_rows=T if hint else 0)   # the hint resizes the launch
     keep = sel["keep_bits"].cpu().numpy().view(np.uint64)
     o = oracle.router_union(keep, h, w, K, threads=8)
     gg = {k: v.cpu().numpy() for k, v in g.items()}
