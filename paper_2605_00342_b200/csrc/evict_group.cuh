@@ -517,18 +517,18 @@ __device__ __forceinline__ void g_select_values(GTree<G> &t, const float (&c)[NP
 // ------------------------------------------------------------ A6
 // Only kept nodes do work, spread over the group by slot so no lane serialises
 // a cluster of kept nodes (kept nodes crowd the low indices):
-//   1. each lane lists its kept nodes: klist[slot] = node (slot = popc(keep below node));
+//   1. klist[slot] = node (slot = popc(keep below node)), built once by the select;
 //   2. slot s (lane s % G) ORs bit s into its parent's child mask (shared atomics);
 //   3. slot s builds its ancestor-or-self row by walking the parent chain of the
 //      shared-memory record (depth steps, no level loop), reads next-token /
 //      next-sibling from the child masks and emits the packed row.
-// par: the tree's shared parent record; child (NMAX × W words) and klist
-// (NMAX bytes): this group's scratch.
+// par: the tree's shared parent record; klist: its kept nodes (built by the select); child (NMAX × W words)
+// (all in shared memory).
 template <int G>
 __device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W], int n, bool emit,
                                        int k, int b, int N, int off, int pos_off,
                                        const int8_t *par, uint64_t *child,
-                                       uint8_t *klist, int32_t *__restrict__ kept_index,
+                                       const uint8_t *klist, int32_t *__restrict__ kept_index,
                                        int32_t *__restrict__ retrieve_index,
                                        int32_t *__restrict__ positions,
                                        int32_t *__restrict__ next_token,
@@ -540,11 +540,6 @@ __device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W]
     const int base = g * NP;
     const int kk = emit ? k : 0;
     if (emit) {
-#pragma unroll
-        for (int r = 0; r < NP; r++) {
-            const int i = base + r;
-            if (i < n && bit_w<W>(keep, i)) klist[popc_below_w<W>(keep, i)] = (uint8_t)i;
-        }
         for (int s = g; s < kk; s += G)
 #pragma unroll
             for (int w = 0; w < W; w++) child[s * W + w] = 0ull;

@@ -287,6 +287,7 @@ struct EmitRec {
     static constexpr int W = grp::GShape<G>::W;
     uint64_t keep[W];
     alignas(8) int8_t par[NMAX];
+    alignas(8) uint8_t klist[NMAX];   // kept nodes, ascending (slot order), built once in A1
     int n, k;
     uint32_t status;
 };
@@ -382,6 +383,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 for (int r = 0; r < grp::NP; r++) pw[r >> 2] |= (uint32_t)(t.par[r] & 0xff) << (8 * (r & 3));
                 *reinterpret_cast<uint2 *>(&er.par[base]) = make_uint2(pw[0], pw[1]);
                 if (g < W) er.keep[g] = t.keep[g];
+#pragma unroll
+                for (int r = 0; r < grp::NP; r++) {
+                    const int i = base + r;
+                    if (i < t.n && grp::bit_w<W>(t.keep, i)) er.klist[grp::popc_below_w<W>(t.keep, i)] = (uint8_t)i;
+                }
                 if (g == 0) { er.n = t.n; er.k = k; er.status = t.status; }
             } else if (g == 0) {
                 s_cnt[slot] = 0;
@@ -422,13 +428,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 EmitRec<G> &er = rec[slot];
                 const int k = er.k;
                 uint32_t st = er.status;
-                uint64_t keep[W];
-#pragma unroll
-                for (int w = 0; w < W; w++) keep[w] = er.keep[w];
-                for (int i = lane; i < er.n; i += 32)
-                    if (grp::bit_w<W>(keep, i)) klist[grp::popc_below_w<W>(keep, i)] = (uint8_t)i;
-                __syncwarp();
-                tree_union<NPL, IDF, KT, EW, CL>(st, klist, k, b, N, L, rt.top_k, E, rt.id_format,
+                tree_union<NPL, IDF, KT, EW, CL>(st, er.klist, k, b, N, L, rt.top_k, E, rt.id_format,
                                                  rt.ids, wscr, Epad, out.union_count, out.union_total,
                                                  out.union_bits, out.expert_hist);
                 if (lane == 0) er.status = st;
@@ -483,10 +483,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
 #pragma unroll
             for (int w = 0; w < W; w++) keep[w] = active ? er.keep[w] : 0ull;
             uint64_t *child = reinterpret_cast<uint64_t *>(wscr) + (size_t)gi * NMAX * W;
-            uint8_t *gklist = wscr + (size_t)TPW * NMAX * W * 8 + (size_t)gi * NMAX;
             grp::g_emit<G>(keep, active ? er.n : 0, active && k > 0, k, b, N, off,
                            (active && out.pos_offset) ? __ldg(out.pos_offset + b) : 0, er.par,
-                           child, gklist, out.kept_index, out.retrieve_index, out.positions,
+                           child, er.klist, out.kept_index, out.retrieve_index, out.positions,
                            out.next_token, out.next_sibling, out.tree_mask);
             __syncwarp();
         }
