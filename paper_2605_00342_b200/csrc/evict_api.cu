@@ -85,7 +85,9 @@ const char *evict_status_string(evict_status_t s)
 size_t evict_workspace_bytes(int32_t batch)
 {
     if (batch < 1) return 0;
-    const size_t ntiles = ((size_t)batch + kTileTrees - 1) / kTileTrees;
+    // one state word per tile of the finer of the two tilings (k_fused: 4-tree warp tiles)
+    const int tt = kTileTrees < kFusedTileTrees ? kTileTrees : kFusedTileTrees;
+    const size_t ntiles = ((size_t)batch + tt - 1) / tt;
     return 8 * (1 + ntiles);
 }
 

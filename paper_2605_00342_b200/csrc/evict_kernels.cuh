@@ -268,18 +268,21 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(evict_trees_t tr, const u
 }
 
 // ------------------------------------------------------------ fused
-// One CTA tile = 32 consecutive trees.  A1–A5 and A6 run sub-warp-per-tree
-// (evict_group.cuh: G lanes per tree, 32/G trees per warp instruction); A7 runs
-// one warp per tree.  Phases per tile:
-//   A1  select every tree of the tile (outputs written) and park an emit record
-//       (parent, depth, keep) in shared memory;
-//   --  barrier; warp 0 scans the 32 row counts and publishes the tile aggregate
-//       (decoupled look-back state);
-//   A2  expert union, one warp per tree, 4 trees per warp;
-//   --  warp 0 looks back for the tile prefix (its wait overlapped A2) and
-//       takes the next tile ticket; barrier;
+// Tiles are per WARP: a warp takes a ticket for kWT = 4 consecutive trees and
+// carries them through every phase with no CTA-wide barrier.  A1–A5 and A6 run
+// sub-warp-per-tree (evict_group.cuh: G lanes per tree); A7 runs one warp per
+// tree.  Phases per warp tile:
+//   A1  select the 4 trees (outputs written), park an emit record (parent,
+//       keep, kept list) in shared memory;
+//   --  publish the tile's row count (decoupled look-back state) and take the
+//       next ticket early;
+//   A2  expert union, one tree at a time;
+//   --  look back for the tile prefix (its wait overlapped A2);
 //   C   verify-tree emit (A6) at the packed offsets.
-constexpr int kTile = 32;
+// Predecessor tiles always belong to warps that took their ticket earlier and
+// are resident, so the look-back cannot deadlock.
+constexpr int kWT = 4;                 // trees per warp tile
+constexpr int kTile = kWarps * kWT;    // records per CTA
 
 template <int G>
 struct EmitRec {
@@ -314,8 +317,7 @@ __host__ __device__ inline size_t fused_smem_bytes(int L, int E, bool flags)
 {
     return (size_t)kWarps * fused_scratch_bytes<G>(L, E, flags)          // scratch
            + align16(sizeof(EmitRec<G>) * kTile)                         // records
-           + (size_t)kWarps * grp::GShape<G>::TPW * grp::GShape<G>::NMAX  // ranks
-           + (size_t)kWarps * 128;                                       // klist
+           + (size_t)kWarps * grp::GShape<G>::TPW * grp::GShape<G>::NMAX; // ranks (order row)
 }
 
 template <int NPL, int IDF, int KT, int EW, int CL>
@@ -328,10 +330,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     constexpr int TPW = grp::GShape<G>::TPW;
     constexpr int NMAX = grp::GShape<G>::NMAX;
     constexpr int W = grp::GShape<G>::W;
-    constexpr int PASSES = kTile / (kWarps * TPW);   // 1 (G=8) or 2 (G=16)
+    constexpr int PASSES = kWT / TPW;                // 1 (G=8) or 2 (G=16)
     constexpr bool FLAGS = IDF == 1 || IDF == 4;
     extern __shared__ __align__(16) uint8_t dsm[];
-    __shared__ int s_cnt[kTile], s_off[kTile], s_tile, s_next;
     const int warp = threadIdx.x >> 5, lane = lane_id();
     const int gi = grp::gidx<G>(), g = grp::gl<G>();
     const int N = tr.max_nodes;
@@ -340,22 +341,22 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     const bool do_union = out.union_count != nullptr;
     const size_t scratch = fused_scratch_bytes<G>(L, E, FLAGS && do_union);
     uint8_t *wscr = dsm + (size_t)warp * scratch;
-    EmitRec<G> *rec = reinterpret_cast<EmitRec<G> *>(dsm + (size_t)kWarps * scratch);
-    uint8_t *ranks = reinterpret_cast<uint8_t *>(rec) + align16(sizeof(EmitRec<G>) * kTile);
+    EmitRec<G> *rec = reinterpret_cast<EmitRec<G> *>(dsm + (size_t)kWarps * scratch) + warp * kWT;
+    uint8_t *ranks = reinterpret_cast<uint8_t *>(dsm + (size_t)kWarps * scratch) + align16(sizeof(EmitRec<G>) * kTile);
     uint8_t *rk = ranks + ((size_t)warp * TPW + gi) * NMAX;
-    uint8_t *klist = ranks + (size_t)kWarps * TPW * NMAX + warp * 128;
     const int Epad = union_epad(E);
     unsigned *ticket = reinterpret_cast<unsigned *>(ws);
     uint64_t *states = ws + 1;
-    if (threadIdx.x == 0) { s_tile = (int)atomicAdd(ticket, 1u); s_next = 0; }
-    __syncthreads();
-    int tile = s_tile;
+    int tile = 0;
+    if (lane == 0) tile = (int)atomicAdd(ticket, 1u);
+    tile = __shfl_sync(kFull, tile, 0);
     while (tile < ntiles) {
+        const int b0 = tile * kWT;
         // ---------------- A1: select, sub-warp per tree
 #pragma unroll 1
         for (int pass = 0; pass < PASSES; pass++) {
-            const int slot = pass * (kWarps * TPW) + warp * TPW + gi;
-            const int b = tile * kTile + slot;
+            const int slot = pass * TPW + gi;
+            const int b = b0 + slot;
             const bool active = b < tr.batch;
             grp::GTree<G> t;
             grp::g_load<G>(t, tr.parent, tr.q, tr.n_nodes, b, N, active);
@@ -368,15 +369,14 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             if (out.order) grp::g_rank_argmax<G>(t, rk, c, N, orow, prow);   // kernel-uniform
             else grp::g_select_values<G>(t, c, N, prow);
             const int k = t.kstar;
+            EmitRec<G> &er = rec[slot];
             if (active) {
                 if (g == 0) {
                     if (out.k_star) out.k_star[b] = t.kstar;
                     if (out.e_hat) out.e_hat[b] = t.ehat;
                     if (out.utility) out.utility[b] = t.util;
-                    s_cnt[slot] = k;
                 }
                 if (out.keep_bits && g < WN) out.keep_bits[(size_t)b * WN + g] = t.keep[g < W ? g : 0];
-                EmitRec<G> &er = rec[slot];
                 const int base = g * grp::NP;
                 uint32_t pw[2] = {0u, 0u};
 #pragma unroll
@@ -390,24 +390,23 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 }
                 if (g == 0) { er.n = t.n; er.k = k; er.status = t.status; }
             } else if (g == 0) {
-                s_cnt[slot] = 0;
+                er.k = 0;
             }
             __syncwarp();
         }
-        // ---------------- tile aggregate
-        __syncthreads();
-        int incl = 0;
-        if (warp == 0) {
-            const int cc = s_cnt[lane];
-            incl = cc;
+        // ---------------- tile aggregate (lanes 0..3 = the tile's trees) + next ticket
+        const int cnt = lane < kWT ? rec[lane].k : 0;
+        int incl = cnt;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int v = __shfl_up_sync(kFull, incl, o);
-                if (lane >= o) incl += v;
-            }
-            s_off[lane] = incl - cc;
-            if (lane == 31) st_release(states + tile, (tile == 0 ? kInc : kAgg) | (uint64_t)incl);
+        for (int o = 1; o < kWT; o <<= 1) {
+            const int v = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += v;
         }
+        const int agg = __shfl_sync(kFull, incl, kWT - 1);
+        int off_local = incl - cnt;
+        if (lane == 0) st_release(states + tile, (tile == 0 ? kInc : kAgg) | (uint64_t)agg);
+        int next = 0;
+        if (lane == 0) next = (int)atomicAdd(ticket, 1u);
         // ---------------- A2: expert union, one warp per tree
         if (do_union) {
             if constexpr (FLAGS) {
@@ -416,62 +415,50 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 for (int i = lane; i < nz; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
                 __syncwarp();
             }
-            // trees are taken dynamically (a warp that drew small k* takes more), so the
-            // barrier after the union waits less on the unluckiest warp
 #pragma unroll 1
-            while (true) {
-                int slot = 0;
-                if (lane == 0) slot = atomicAdd(&s_next, 1);
-                slot = __shfl_sync(kFull, slot, 0);
-                const int b = tile * kTile + slot;
-                if (slot >= kTile || b >= tr.batch) break;
+            for (int slot = 0; slot < kWT; slot++) {
+                const int b = b0 + slot;
+                if (b >= tr.batch) break;
                 EmitRec<G> &er = rec[slot];
-                const int k = er.k;
                 uint32_t st = er.status;
-                tree_union<NPL, IDF, KT, EW, CL>(st, er.klist, k, b, N, L, rt.top_k, E, rt.id_format,
+                tree_union<NPL, IDF, KT, EW, CL>(st, er.klist, er.k, b, N, L, rt.top_k, E, rt.id_format,
                                                  rt.ids, wscr, Epad, out.union_count, out.union_total,
                                                  out.union_bits, out.expert_hist);
                 if (lane == 0) er.status = st;
                 __syncwarp();
             }
         }
-        // ---------------- look-back for the tile prefix + next ticket
-        if (warp == 0) {
-            const int agg = __shfl_sync(kFull, incl, 31);
-            unsigned prefix = 0;
-            if (tile > 0) {
-                int end = tile;
-                while (true) {
-                    const int j = end - 1 - lane;
-                    const uint64_t sv = j >= 0 ? ld_acquire(states + j) : kInc;
-                    const unsigned flag = (unsigned)(sv >> 62);
-                    const unsigned inc_mask = __ballot_sync(kFull, flag == 2);
-                    const unsigned zero_mask = __ballot_sync(kFull, flag == 0);
-                    const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
-                    const unsigned before = first_inc == 32 ? kFull : ((1u << first_inc) - 1u);
-                    if (zero_mask & before) continue;
-                    const unsigned v = lane <= first_inc ? (unsigned)(sv & kValMask) : 0u;
-                    prefix += __reduce_add_sync(kFull, v);
-                    if (first_inc < 32) break;
-                    end -= 32;
-                }
-                if (lane == 0) st_release(states + tile, kInc | (uint64_t)(prefix + (unsigned)agg));
+        // ---------------- look-back for the tile prefix
+        unsigned prefix = 0;
+        if (tile > 0) {
+            int end = tile;
+            while (true) {
+                const int j = end - 1 - lane;
+                const uint64_t sv = j >= 0 ? ld_acquire(states + j) : kInc;
+                const unsigned flag = (unsigned)(sv >> 62);
+                const unsigned inc_mask = __ballot_sync(kFull, flag == 2);
+                const unsigned zero_mask = __ballot_sync(kFull, flag == 0);
+                const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
+                const unsigned before = first_inc == 32 ? kFull : ((1u << first_inc) - 1u);
+                if (zero_mask & before) continue;
+                const unsigned v = lane <= first_inc ? (unsigned)(sv & kValMask) : 0u;
+                prefix += __reduce_add_sync(kFull, v);
+                if (first_inc < 32) break;
+                end -= 32;
             }
-            s_off[lane] += (int)prefix;
-            if (lane == 0) s_tile = (int)atomicAdd(ticket, 1u);
+            if (lane == 0) st_release(states + tile, kInc | (uint64_t)(prefix + (unsigned)agg));
         }
-        __syncthreads();
-        const int next = s_tile;
-        if (threadIdx.x == 0) s_next = 0;   // every warp has left this tile's union loop
+        off_local += (int)prefix;
+        next = __shfl_sync(kFull, next, 0);
         // ---------------- C: verify-tree emit, sub-warp per tree
 #pragma unroll 1
         for (int pass = 0; pass < PASSES; pass++) {
-            const int slot = pass * (kWarps * TPW) + warp * TPW + gi;
-            const int b = tile * kTile + slot;
+            const int slot = pass * TPW + gi;
+            const int b = b0 + slot;
             const bool active = b < tr.batch;
             const EmitRec<G> &er = rec[slot];
             const int k = active ? er.k : 0;
-            const int off = s_off[slot];
+            const int off = __shfl_sync(kFull, off_local, slot);
             if (active && g == 0) {
                 if (out.status) out.status[b] = er.status;
                 if (out.verify_offsets) {

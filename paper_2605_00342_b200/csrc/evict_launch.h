@@ -22,7 +22,7 @@
 
 namespace evict {
 constexpr int kTileTrees = 8;        // trees per CTA tile of k_build (= warps per CTA)
-constexpr int kFusedTileTrees = 32;  // trees per CTA tile of k_fused (4 per warp)
+constexpr int kFusedTileTrees = 4;   // trees per warp tile of k_fused
 int dev_sms();
 template <int NPL> evict_status_t launch_select(EVICT_SELECT_ARGS);
 template <int NPL> evict_status_t launch_build(EVICT_BUILD_ARGS);
