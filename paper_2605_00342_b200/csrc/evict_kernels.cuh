@@ -320,12 +320,16 @@ __host__ __device__ inline size_t fused_smem_bytes(int L, int E, bool flags)
            + (size_t)kWarps * grp::GShape<G>::TPW * grp::GShape<G>::NMAX; // ranks (order row)
 }
 
-template <int NPL, int IDF, int KT, int EW, int CL>
+// LEAN: the serving / bench configuration (u8 top-8 ids, E = 128, no order row, no
+// union bit rows, no histogram) compiled without the other paths — with warps in
+// different phases the full kernel's code footprint thrashes the instruction cache.
+template <int NPL, int IDF, int KT, int EW, int CL, bool LEAN = false>
 __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, const float *cost,
                                                        int cost_stride, evict_routing_t rt,
                                                        evict_fused_out_t out, uint64_t *ws,
                                                        int ntiles)
 {
+    static_assert(!LEAN || IDF == 1, "LEAN is the u8 top-8 configuration");
     constexpr int G = NPL == 2 ? 8 : 16;
     constexpr int TPW = grp::GShape<G>::TPW;
     constexpr int NMAX = grp::GShape<G>::NMAX;
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             grp::g_levels<G, true>(t, sd);
             int32_t *orow = (active && out.order) ? out.order + (size_t)b * N : nullptr;
             float *prow = (active && out.prefix_sums) ? out.prefix_sums + (size_t)b * N : nullptr;
-            if (out.order) grp::g_rank_argmax<G>(t, rk, c, N, orow, prow);   // kernel-uniform
+            if (!LEAN && out.order) grp::g_rank_argmax<G>(t, rk, c, N, orow, prow);   // kernel-uniform
             else grp::g_select_values<G>(t, c, N, prow);
             const int k = t.kstar;
             EmitRec<G> &er = rec[slot];
@@ -421,9 +425,13 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 if (b >= tr.batch) break;
                 EmitRec<G> &er = rec[slot];
                 uint32_t st = er.status;
-                tree_union<NPL, IDF, KT, EW, CL>(st, er.klist, er.k, b, N, L, rt.top_k, E, rt.id_format,
-                                                 rt.ids, wscr, Epad, out.union_count, out.union_total,
-                                                 out.union_bits, out.expert_hist);
+                if constexpr (LEAN)
+                    tree_union_flags64<1, CL, true, false>(st, er.klist, er.k, b, N, L, E, rt.ids, wscr,
+                                                           out.union_count, out.union_total, nullptr);
+                else
+                    tree_union<NPL, IDF, KT, EW, CL>(st, er.klist, er.k, b, N, L, rt.top_k, E, rt.id_format,
+                                                     rt.ids, wscr, Epad, out.union_count, out.union_total,
+                                                     out.union_bits, out.expert_hist);
                 if (lane == 0) er.status = st;
                 __syncwarp();
             }
@@ -599,7 +607,11 @@ struct FusedLauncher {
                               const evict_routing_t *rt, const evict_fused_out_t *o, uint64_t *ws,
                               int ntiles, cudaStream_t s)
     {
-        auto kern = k_fused<NPL, IDF, KT, EW, CL>;
+        auto kern = k_fused<NPL, IDF, KT, EW, CL, false>;
+        if constexpr (IDF == 1 && EW == 2) {
+            if (rt->num_experts == 128 && !o->order && !o->union_bits && !o->expert_hist && o->union_count)
+                kern = k_fused<NPL, IDF, KT, EW, CL, true>;
+        }
         constexpr int G = NPL == 2 ? 8 : 16;
         const size_t dyn = fused_smem_bytes<G>(rt->num_layers, rt->num_experts,
                                                (IDF == 1 || IDF == 4) && o->union_count);
