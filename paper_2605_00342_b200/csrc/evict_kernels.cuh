@@ -301,8 +301,17 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(siz
 template <int G>
 __host__ __device__ constexpr size_t fused_scratch_fixed()
 {
+    // sweeps: TPW × (NMAX + 8) floats; emit: TPW × NMAX × W child words (+ slack)
     return align16(grp::GShape<G>::TPW * grp::GShape<G>::NMAX *
                    (sizeof(int2) > 2 * 8 * grp::GShape<G>::W ? sizeof(int2) : 2 * 8 * grp::GShape<G>::W));
+}
+// bytes of the scratch the sweeps (padded score arrays) and emit (child masks) write
+template <int G>
+__host__ __device__ constexpr size_t fused_scratch_dirty()
+{
+    constexpr size_t sw = (size_t)grp::GShape<G>::TPW * (grp::GShape<G>::NMAX + 8) * 4;
+    constexpr size_t ch = (size_t)grp::GShape<G>::TPW * grp::GShape<G>::NMAX * grp::GShape<G>::W * 8;
+    return align16(sw > ch ? sw : ch);
 }
 __host__ __device__ inline int union_epad(int E) { return E <= 128 ? 128 : 256; }
 template <int G>
@@ -354,6 +363,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     int tile = 0;
     if (lane == 0) tile = (int)atomicAdd(ticket, 1u);
     tile = __shfl_sync(kFull, tile, 0);
+    bool first = true;
     while (tile < ntiles) {
         const int b0 = tile * kWT;
         // ---------------- A1: select, sub-warp per tree
@@ -366,7 +376,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             grp::g_load<G>(t, tr.parent, tr.q, tr.n_nodes, b, N, active);
             float c[grp::NP];
             grp::g_load_cost<G>(c, t, cost + (size_t)(active ? b : 0) * cost_stride, N);
-            float *sd = reinterpret_cast<float *>(wscr) + gi * NMAX;
+            // per-tree score arrays 8 floats apart in bank space: the 4 trees' reads of
+            // their roots (and other equal node ids) land on different banks
+            float *sd = reinterpret_cast<float *>(wscr) + gi * (NMAX + 8);
             grp::g_levels<G, true>(t, sd);
             int32_t *orow = (active && out.order) ? out.order + (size_t)b * N : nullptr;
             float *prow = (active && out.prefix_sums) ? out.prefix_sums + (size_t)b * N : nullptr;
@@ -414,10 +426,15 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
         // ---------------- A2: expert union, one warp per tree
         if (do_union) {
             if constexpr (FLAGS) {
+                // every union path leaves its flag block zero after each tree; only the
+                // prefix the sweeps / emit scribbled on needs clearing (all of it once)
                 uint4 *f4 = reinterpret_cast<uint4 *>(wscr);
-                const int nz = union_flag_bytes(L, E) / 16;   // uint4 words
+                const int nflag = union_flag_bytes(L, E) / 16;   // uint4 words
+                constexpr int dirty = (int)(fused_scratch_dirty<G>() / 16);
+                const int nz = first ? nflag : (dirty < nflag ? dirty : nflag);
                 for (int i = lane; i < nz; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
                 __syncwarp();
+                first = false;
             }
 #pragma unroll 1
             for (int slot = 0; slot < kWT; slot++) {
