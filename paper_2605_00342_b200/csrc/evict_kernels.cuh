@@ -364,6 +364,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     if (lane == 0) tile = (int)atomicAdd(ticket, 1u);
     tile = __shfl_sync(kFull, tile, 0);
     bool first = true;
+    int epoch = 0;   // LEAN union marker window (tree_union_flags64)
     while (tile < ntiles) {
         const int b0 = tile * kWT;
         // ---------------- A1: select, sub-warp per tree
@@ -444,7 +445,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 uint32_t st = er.status;
                 if constexpr (LEAN)
                     tree_union_flags64<1, CL, true, false>(st, er.klist, er.k, b, N, L, E, rt.ids, wscr,
-                                                           out.union_count, out.union_total, nullptr);
+                                                           out.union_count, out.union_total, nullptr,
+                                                           &epoch);
                 else
                     tree_union<NPL, IDF, KT, EW, CL>(st, er.klist, er.k, b, N, L, rt.top_k, E, rt.id_format,
                                                      rt.ids, wscr, Epad, out.union_count, out.union_total,

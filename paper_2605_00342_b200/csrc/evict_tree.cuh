@@ -1096,10 +1096,17 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                                                    int b, int N, int L, int E, const void *__restrict__ ids,
                                                    uint8_t *flags, int32_t *__restrict__ union_count,
                                                    int32_t *__restrict__ union_total,
-                                                   uint64_t *__restrict__ union_bits)
+                                                   uint64_t *__restrict__ union_bits, int *epoch = nullptr)
 {
     static_assert(IDF == 1 || IDF == 4, "flag union takes u8 or i32 ids");
     constexpr int PASSES = (R + 3) / 4;
+    // Marker mode (single pass, no bit rows, caller keeps `epoch`): tree t stores the
+    // byte 1 << (t mod 4) and counts only that bit, so the block is cleared once per 4
+    // trees instead of after every tree (a byte holds its last writer's marker; the 4
+    // markers of a window are distinct).  Otherwise: store 1, clear after each read.
+    const bool mark = PASSES == 1 && !BITS && epoch != nullptr;
+    const int ep = mark ? *epoch : 0;
+    const uint32_t marker = 1u << ep;
     constexpr int RP = R < 4 ? R : 4;                  // rounds per pass
     constexpr int U = IDF == 1 ? 4 : 1;                // nodes per load batch (i32 rows are 4x wider)
     const int lane = lane_id();
@@ -1156,13 +1163,13 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                             }
 #pragma unroll
                             for (int qb = 0; qb < 4; qb++)
-                                sts_u8((__byte_perm(wm, 0, 0x4440 | qb) << 6) + (lbase + cc), 1u);
+                                sts_u8((__byte_perm(wm, 0, 0x4440 | qb) << 6) + (lbase + cc), marker);
                         } else {
 #pragma unroll
                             for (int qb = 0; qb < 4; qb++) {
                                 const uint32_t e = v[u][cc][qb];
                                 bad |= e >= (uint32_t)E;
-                                sts_u8(((e & 127u) << 6) + (lbase + cc), 1u);
+                                sts_u8(((e & 127u) << 6) + (lbase + cc), marker);
                             }
                         }
                     }
@@ -1191,11 +1198,24 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
             const int q = lane & 3, p8 = lane >> 2;
             const uint32_t fw = fbase + 16u * (uint32_t)(p8 * 4 + q);
             uint32_t a0 = 0u, a1 = 0u, a2 = 0u, a3 = 0u;
+            if (mark) {
+                // byte sums of marker bits ≤ 16·8 = 128 per lane: no carry into the next byte
+                const uint32_t mk = 0x01010101u << ep;
+                const bool wrap = ep == 3;
 #pragma unroll
-            for (int i = 0; i < 16; i++) {
-                const uint4 x = lds_v4(fw + 512u * i);
-                a0 += x.x; a1 += x.y; a2 += x.z; a3 += x.w;
-                sts_v4_zero(fw + 512u * i);
+                for (int i = 0; i < 16; i++) {
+                    const uint4 x = lds_v4(fw + 512u * i);
+                    a0 += x.x & mk; a1 += x.y & mk; a2 += x.z & mk; a3 += x.w & mk;
+                    if (wrap) sts_v4_zero(fw + 512u * i);
+                }
+                a0 >>= ep; a1 >>= ep; a2 >>= ep; a3 >>= ep;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; i++) {
+                    const uint4 x = lds_v4(fw + 512u * i);
+                    a0 += x.x; a1 += x.y; a2 += x.z; a3 += x.w;
+                    sts_v4_zero(fw + 512u * i);
+                }
             }
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
@@ -1231,6 +1251,7 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
         tot = 0;
     }
     __syncwarp();
+    if (mark && run) *epoch = (ep + 1) & 3;   // the block was cleared when ep == 3
     tot = __reduce_add_sync(kFull, tot);
     if (union_total && lane == 0) union_total[b] = tot;
 }
