@@ -66,17 +66,48 @@ def hbm_peak():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region: an NVML thread polling
+    every 2 ms (a K-step region can last only tens of ms), nvidia-smi -lms 100 as fallback."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.proc = None
+        self.thread = None
+        self.rows = []
+        self.active = False
 
     def start(self):
+        try:
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.stop_evt = threading.Event()
+
+            def run():
+                while not self.stop_evt.is_set():
+                    if self.active:
+                        try:
+                            sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                            self.rows.append((sm, mx, ["Active" if r & bt else "Not Active" for bt in bits]))
+                        except Exception:
+                            pass
+                    time.sleep(0.002)
+
+            self.thread = threading.Thread(target=run, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
@@ -85,31 +116,39 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def region(self, on):
+        """Mark the timed region (the NVML thread only records samples inside it)."""
+        self.active = on
+
     def stop(self):
-        if self.proc is None:
-            return None
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except Exception:
-            self.proc.kill()
-            out = ""
         rows = []
-        for line in out.strip().splitlines():
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 8:
-                continue
+        if self.thread is not None:
+            self.active = False
+            self.stop_evt.set()
+            self.thread.join(timeout=2)
+            rows = self.rows
+        elif self.proc is not None:
+            self.proc.terminate()
             try:
-                rows.append((float(f[0]), float(f[1]), f[4:8]))
-            except ValueError:
-                continue
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            for line in out.strip().splitlines():
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 8:
+                    continue
+                try:
+                    rows.append((float(f[0]), float(f[1]), f[4:8]))
+                except ValueError:
+                    continue
         if not rows:
             return None
         sm = sorted(r[0] for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
+        reasons = sorted({self.NAMES[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": reasons, "samples": len(rows)}
+                "reasons": reasons, "samples": len(rows),
+                "source": "nvml 2 ms" if self.thread is not None else "nvidia-smi 100 ms"}
 
 
 # ------------------------------------------------------------------ algorithmic bytes
@@ -401,11 +440,13 @@ def run_native(args, rank, world, local_rank):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    clk.region(True)
     t0.record(stream)
     for i in range(K):
         step(*evs[i])
     t1.record(stream)
     torch.cuda.synchronize()
+    clk.region(False)
     if world > 1:
         dist.barrier()
     clocks = clk.stop()

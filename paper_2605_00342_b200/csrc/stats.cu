@@ -10,13 +10,14 @@
 namespace evict {
 // ------------------------------------------------------------ stats
 // Scalars (k*, n, status, e_hat, utility) and the k* histogram: one thread per
-// tree (coalesced), block partials in shared memory.  Per-layer union sums:
-// one warp per tree row with lane = layer (coalesced row reads), register
-// accumulators, one atomic per layer per warp at the end — never one shared
-// atomic per (tree, layer).
-__global__ void k_stats(int B, int N, int L, const int32_t *n_nodes, const int32_t *k_star,
-                        const float *e_hat, const float *utility, const int32_t *union_count,
-                        const uint32_t *status, unsigned long long *stats, double *dstats)
+// tree (coalesced); histogram increments are warp-aggregated (__match_any_sync:
+// one shared atomic per distinct bin per warp, not per tree).  Per-layer union
+// sums: one warp per tree row with lane = layer (coalesced row reads), 4 rows in
+// flight per warp, register accumulators, one atomic per layer per warp at the end.
+__global__ void __launch_bounds__(256) k_stats(int B, int N, int L, const int32_t *n_nodes, const int32_t *k_star,
+                                               const float *e_hat, const float *utility,
+                                               const int32_t *union_count, const uint32_t *status,
+                                               unsigned long long *stats, double *dstats)
 {
     extern __shared__ unsigned long long sh[];  // [6 + N + L]
     const int len = 6 + N + L;
@@ -24,36 +25,53 @@ __global__ void k_stats(int B, int N, int L, const int32_t *n_nodes, const int32
     __shared__ double sd[2];
     if (threadIdx.x < 2) sd[threadIdx.x] = 0.0;
     __syncthreads();
+    const int lane = threadIdx.x & 31;
     unsigned long long nt = 0, sk = 0, sn = 0, su = 0, sbad = 0;
     double de = 0.0, du = 0.0;
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
-        nt++;
-        if (status && status[b]) {
-            sbad++;
-            atomicAdd(&sh[5], 1ull);
-            continue;
+    const int stride = gridDim.x * blockDim.x;
+    for (int b0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); b0 < B; b0 += stride) {
+        const int b = b0 + lane;                       // warp-uniform loop, lane-valid trees
+        const bool in = b < B;
+        const bool bad = in && status && status[b];
+        const int k = (in && !bad) ? k_star[b] : 0;
+        if (in) {
+            nt++;
+            if (bad) {
+                sbad++;
+            } else {
+                sk += k;
+                sn += n_nodes ? n_nodes[b] : N;
+                de += e_hat[b];
+                du += utility[b];
+            }
         }
-        const int k = k_star[b];
-        sk += k;
-        sn += n_nodes ? n_nodes[b] : N;
-        atomicAdd(&sh[5 + k], 1ull);
-        de += e_hat[b];
-        du += utility[b];
+        // histogram bin 0 = errored trees, k otherwise; warp-aggregated
+        const int bin = in ? (bad ? 0 : k) : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+        if (in && lane == __ffs(peers) - 1) atomicAdd(&sh[5 + bin], (unsigned long long)__popc(peers));
     }
-    // per-layer sums: warp per tree row
-    const int lane = threadIdx.x & 31;
+    // per-layer sums: warp per tree row, 4 rows in flight
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
     if (L > 0) {
-        for (int b = gw; b < B; b += nw) {
-            if (status && status[b]) continue;
-            const int32_t *row = union_count + (size_t)b * L;
+        for (int b = gw; b < B; b += 4 * nw) {
+            int32_t v[4][4];
 #pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const int l = lane + 32 * c;
-                if (l < L) acc[c] += (unsigned long long)__ldg(row + l);
+            for (int u = 0; u < 4; u++) {
+                const int bu = b + u * nw;
+                const bool ok = bu < B && !(status && status[bu]);
+                const int32_t *row = union_count + (size_t)(ok ? bu : 0) * L;
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    const int l = lane + 32 * c;
+                    v[u][c] = (ok && l < L) ? __ldg(row + l) : 0;
+                }
             }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+#pragma unroll
+                for (int c = 0; c < 4; c++) acc[c] += (unsigned long long)v[u][c];
         }
 #pragma unroll
         for (int c = 0; c < 4; c++) {
@@ -110,7 +128,7 @@ extern "C" evict_status_t evict_batch_stats(int32_t batch, int32_t max_nodes, in
     if (cudaMemsetAsync(stats, 0, sizeof(int64_t) * len, s) != cudaSuccess) return EVICT_ERR_CUDA;
     if (cudaMemsetAsync(dstats, 0, sizeof(double) * 2, s) != cudaSuccess) return EVICT_ERR_CUDA;
     int blocks = (batch + 255) / 256;
-    if (blocks > sms * 2) blocks = sms * 2;
+    if (blocks > sms * 8) blocks = sms * 8;   // 64 warps per SM of loads in flight
     evict::k_stats<<<blocks, 256, sizeof(unsigned long long) * len, s>>>(
         batch, max_nodes, num_layers, n_nodes, k_star, e_hat, utility, union_count, status,
         reinterpret_cast<unsigned long long *>(stats), dstats);
