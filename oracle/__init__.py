@@ -57,6 +57,9 @@ def lib():
             vp = ctypes.c_void_p
             L.oracle_select_batch.argtypes = [ctypes.c_int] * 3 + [vp] * 4 + [ctypes.c_int] + [vp] * 11
             L.oracle_select_batch.restype = None
+            L.oracle_select_batch_policy.argtypes = ([ctypes.c_int] * 3 + [vp] * 4 + [ctypes.c_int] * 2 +
+                                                     [ctypes.c_double, ctypes.c_int] + [vp] * 11)
+            L.oracle_select_batch_policy.restype = None
             L.oracle_build_batch.argtypes = [ctypes.c_int] * 2 + [vp] * 11
             L.oracle_build_batch.restype = None
             L.oracle_union_batch.argtypes = [ctypes.c_int] * 3 + [vp] * 3 + [ctypes.c_int] * 4 + [vp] * 4
@@ -85,8 +88,20 @@ def _ranges(B, threads):
     return [(s, min(B, s + step)) for s in range(0, B, step)]
 
 
-def select(parent, q, cost, n_nodes=None, cost_stride=0, threads=1):
-    """A1–A5 for a [B][N] batch.  Returns a dict of numpy arrays."""
+POLICIES = {"cost": 0, "coverage": 1, "fixed": 2}
+
+
+def select(parent, q, cost, n_nodes=None, cost_stride=0, threads=1, policy=None):
+    """A1–A5 for a [B][N] batch.  Returns a dict of numpy arrays.
+    policy: None / ("cost",) — Eq. 10; ("coverage", rho) — smallest k with S_k/S_K ≥ rho
+    (PAPER.md:290-291); ("fixed", k) — k* = min(k, n_b)."""
+    kind, rho, kfix = 0, 0.0, 0
+    if policy is not None:
+        kind = POLICIES[policy[0]]
+        if kind == 1:
+            rho = float(np.float32(policy[1]))   # the GPU receives ρ as fp32
+        elif kind == 2:
+            kfix = int(policy[1])
     parent = _c(parent, np.int32)
     q = _c(q, np.float32)
     cost = _c(cost, np.float32)
@@ -102,8 +117,9 @@ def select(parent, q, cost, n_nodes=None, cost_stride=0, threads=1):
     L = lib()
 
     def run(r):
-        L.oracle_select_batch(r[0], r[1], N, _ptr(n_nodes), _ptr(parent), _ptr(q), _ptr(cost),
-                              cost_stride, _ptr(out["score"]), _ptr(out["depth"]),
+        L.oracle_select_batch_policy(r[0], r[1], N, _ptr(n_nodes), _ptr(parent), _ptr(q), _ptr(cost),
+                              cost_stride, kind, rho, kfix,
+                              _ptr(out["score"]), _ptr(out["depth"]),
                               _ptr(out["order"]), _ptr(out["S"]), _ptr(out["R"]),
                               _ptr(out["k_star"]), _ptr(out["e_hat"]), _ptr(out["utility"]),
                               _ptr(out["keep_bits"]), _ptr(out["tie_bits"]), _ptr(out["status"]))

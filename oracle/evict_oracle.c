@@ -117,12 +117,49 @@ static void rank_nodes(int n, const float *score, int32_t *order)
  * Arrays S, R, score, depth, order have room for n entries; keep_bits and
  * tie_bits have W = ceil(max_nodes/64) words.  On a data error every output
  * is written in its defined error state (k*=0, keep=0, S=R=0).          */
+/* Selection policies (the cut k* on the same ranking and prefix sums):
+ *   ORACLE_POLICY_COST     k* = smallest argmax S[k]/C(k) (Eq. 10, EVICT)
+ *   ORACLE_POLICY_COVERAGE k* = smallest k with S_k/S_K ≥ ρ, K = n_b: the
+ *                          score-coverage ablation (PAPER.md:290-291,
+ *                          §5.4 "Ablating Cost-Aware Selection"); ρ = 1 is
+ *                          EAGLE-3 (every node under the budget is verified,
+ *                          PAPER.md:292).  If no k qualifies (ρ > 1), k* = n.
+ *                          Near ties: k with |S_k/S_K − ρ| ≤ 1e-5·ρ, and the
+ *                          k after each (a GPU on the other side of ρ).
+ *   ORACLE_POLICY_FIXED    k* = min(k_fixed, n_b): a fixed verify budget on
+ *                          the same ranking.
+ * e_hat = S[k*] and utility = S[k*]/C(k*) for every policy.             */
+#define ORACLE_POLICY_COST 0
+#define ORACLE_POLICY_COVERAGE 1
+#define ORACLE_POLICY_FIXED 2
+
+uint32_t oracle_select_tree_policy(int n, int max_nodes, const int32_t *parent,
+                                   const float *q, const float *cost,
+                                   int policy, double rho, int k_fixed,
+                                   float *score, int32_t *depth, int32_t *order,
+                                   double *S, double *R, int32_t *k_star,
+                                   double *e_hat, double *utility,
+                                   uint64_t *keep_bits, uint64_t *tie_bits, int W);
+
 uint32_t oracle_select_tree(int n, int max_nodes, const int32_t *parent,
                             const float *q, const float *cost,
                             float *score, int32_t *depth, int32_t *order,
                             double *S, double *R, int32_t *k_star,
                             double *e_hat, double *utility,
                             uint64_t *keep_bits, uint64_t *tie_bits, int W)
+{
+    return oracle_select_tree_policy(n, max_nodes, parent, q, cost, ORACLE_POLICY_COST, 0.0, 0,
+                                     score, depth, order, S, R, k_star, e_hat, utility,
+                                     keep_bits, tie_bits, W);
+}
+
+uint32_t oracle_select_tree_policy(int n, int max_nodes, const int32_t *parent,
+                                   const float *q, const float *cost,
+                                   int policy, double rho, int k_fixed,
+                                   float *score, int32_t *depth, int32_t *order,
+                                   double *S, double *R, int32_t *k_star,
+                                   double *e_hat, double *utility,
+                                   uint64_t *keep_bits, uint64_t *tie_bits, int W)
 {
     for (int w = 0; w < W; w++) { keep_bits[w] = 0; tie_bits[w] = 0; }
     *k_star = 0; *e_hat = 0.0; *utility = 0.0;
@@ -146,8 +183,17 @@ uint32_t oracle_select_tree(int n, int max_nodes, const int32_t *parent,
         R[k - 1] = S[k - 1] / (double)cost[k - 1];   /* +inf cost ⇒ R = 0 */
     }
     int kbest = 1;
-    for (int k = 2; k <= n; k++)
-        if (R[k - 1] > R[kbest - 1]) kbest = k;      /* strict: smallest k */
+    if (policy == ORACLE_POLICY_COVERAGE) {
+        double SK = S[n - 1];
+        kbest = n;
+        for (int k = 1; k <= n; k++)
+            if (S[k - 1] / SK >= rho) { kbest = k; break; }
+    } else if (policy == ORACLE_POLICY_FIXED) {
+        kbest = k_fixed < n ? k_fixed : n;
+    } else {
+        for (int k = 2; k <= n; k++)
+            if (R[k - 1] > R[kbest - 1]) kbest = k;      /* strict: smallest k */
+    }
 
     *k_star = kbest;
     *e_hat = S[kbest - 1];
@@ -156,14 +202,36 @@ uint32_t oracle_select_tree(int n, int max_nodes, const int32_t *parent,
         int v = order[j];
         keep_bits[v / 64] |= (uint64_t)1 << (v % 64);
     }
-    double band = R[kbest - 1] * (1.0 - ORACLE_TIE_REL);
-    for (int k = 1; k <= n; k++)
-        if (R[k - 1] >= band) tie_bits[(k - 1) / 64] |= (uint64_t)1 << ((k - 1) % 64);
+    if (policy == ORACLE_POLICY_COVERAGE) {
+        double SK = S[n - 1];
+        tie_bits[(kbest - 1) / 64] |= (uint64_t)1 << ((kbest - 1) % 64);
+        for (int k = 1; k <= n; k++) {
+            if (fabs(S[k - 1] / SK - rho) <= ORACLE_TIE_REL * rho) {
+                tie_bits[(k - 1) / 64] |= (uint64_t)1 << ((k - 1) % 64);
+                if (k < n) tie_bits[k / 64] |= (uint64_t)1 << (k % 64);
+            }
+        }
+    } else if (policy == ORACLE_POLICY_FIXED) {
+        tie_bits[(kbest - 1) / 64] |= (uint64_t)1 << ((kbest - 1) % 64);
+    } else {
+        double band = R[kbest - 1] * (1.0 - ORACLE_TIE_REL);
+        for (int k = 1; k <= n; k++)
+            if (R[k - 1] >= band) tie_bits[(k - 1) / 64] |= (uint64_t)1 << ((k - 1) % 64);
+    }
     return 0;
 }
 
 /* Batched wrapper: trees [b_begin, b_end) of a [B][N] batch.
  * cost_stride 0 ⇒ one shared table.  Per-tree arrays are [B][N].       */
+void oracle_select_batch_policy(int b_begin, int b_end, int N, const int32_t *n_nodes,
+                                const int32_t *parent, const float *q,
+                                const float *cost, int cost_stride,
+                                int policy, double rho, int k_fixed,
+                                float *score, int32_t *depth, int32_t *order,
+                                double *S, double *R, int32_t *k_star, double *e_hat,
+                                double *utility, uint64_t *keep_bits,
+                                uint64_t *tie_bits, uint32_t *status);
+
 void oracle_select_batch(int b_begin, int b_end, int N, const int32_t *n_nodes,
                          const int32_t *parent, const float *q,
                          const float *cost, int cost_stride,
@@ -171,6 +239,20 @@ void oracle_select_batch(int b_begin, int b_end, int N, const int32_t *n_nodes,
                          double *S, double *R, int32_t *k_star, double *e_hat,
                          double *utility, uint64_t *keep_bits,
                          uint64_t *tie_bits, uint32_t *status)
+{
+    oracle_select_batch_policy(b_begin, b_end, N, n_nodes, parent, q, cost, cost_stride,
+                               ORACLE_POLICY_COST, 0.0, 0, score, depth, order, S, R, k_star,
+                               e_hat, utility, keep_bits, tie_bits, status);
+}
+
+void oracle_select_batch_policy(int b_begin, int b_end, int N, const int32_t *n_nodes,
+                                const int32_t *parent, const float *q,
+                                const float *cost, int cost_stride,
+                                int policy, double rho, int k_fixed,
+                                float *score, int32_t *depth, int32_t *order,
+                                double *S, double *R, int32_t *k_star, double *e_hat,
+                                double *utility, uint64_t *keep_bits,
+                                uint64_t *tie_bits, uint32_t *status)
 {
     int W = (N + 63) / 64;
     for (int b = b_begin; b < b_end; b++) {
@@ -181,8 +263,8 @@ void oracle_select_batch(int b_begin, int b_end, int N, const int32_t *n_nodes,
             score[o + i] = 0.0f; depth[o + i] = -1; order[o + i] = -1;
             S[o + i] = 0.0; R[o + i] = 0.0;
         }
-        status[b] = oracle_select_tree(n, N, parent + o, q + o,
-                                       cost + (size_t)b * cost_stride,
+        status[b] = oracle_select_tree_policy(n, N, parent + o, q + o,
+                                       cost + (size_t)b * cost_stride, policy, rho, k_fixed,
                                        score + o, depth + o, order + o, S + o,
                                        R + o, &k_star[b], &e_hat[b],
                                        &utility[b], keep_bits + (size_t)b * W,

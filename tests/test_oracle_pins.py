@@ -522,3 +522,86 @@ def test_batch_stats_sums():
     assert s[5:6 + N].sum() == B and s[5] == 2
     assert np.bincount(k[good], minlength=N + 1)[1:].tolist() == s[6:6 + N].tolist()
     assert d[0] == pytest.approx(eh[good].sum()) and d[1] == pytest.approx(ut[good].sum())
+
+
+# ----------------------------------------------------------- policies (NEXT-2)
+def select1p(parent, q, cost, policy):
+    n = len(parent)
+    P = np.full((1, n), -1, np.int32)
+    Q = np.zeros((1, n), np.float32)
+    P[0], Q[0] = parent, q
+    return oracle.select(P, Q, np.asarray(cost, np.float32), n_nodes=np.array([n], np.int32),
+                         policy=policy)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_coverage_policy_bruteforce(seed):
+    """k* = the smallest prefix with S_k/S_K ≥ ρ.  Independently of the
+    oracle's ranking: the smallest size m for which SOME ancestor-closed subset reaches
+    ρ·S_total (exact rationals; dyadic q keeps fp32 scores exact)."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(1, 12))
+    parent, q = rand_tree(rng, n, dyadic=8)
+    sc = exact_scores(parent, q)
+    best, _ = best_sum_per_size(parent, sc)
+    total = sum(sc)
+    for rho in (0.05, 0.4, 0.7, 0.9, 1.0):
+        r = Fraction(float(np.float32(rho)))
+        m = min(k for k in range(1, n + 1) if best[k] >= r * total)
+        o = select1p(parent, q, np.ones(n), ("coverage", rho))
+        assert o["status"][0] == 0
+        ties = [k + 1 for k in range(n) if (int(o["tie_bits"][0, 0]) >> k) & 1]
+        assert o["k_star"][0] == m or (m in ties and o["k_star"][0] in ties), (rho, m, o["k_star"][0])
+        kept = keep_set(o["keep_bits"][0], n)
+        assert len(kept) == o["k_star"][0] and is_ancestor_closed(parent, kept)
+        assert sum(sc[v] for v in kept) == best[len(kept)]
+
+
+def test_coverage_rho_one_is_eagle3_full_tree():
+    """ρ = 1 verifies every node under the budget (EAGLE-3): k* = the number of
+    nodes with a positive score (zero-score nodes add nothing to S_K and rank last)."""
+    rng = np.random.default_rng(7)
+    for _ in range(40):
+        n = int(rng.integers(1, 40))
+        parent, q = rand_tree(rng, n, dyadic=4)
+        o = select1p(parent, q, np.ones(n), ("coverage", 1.0))
+        pos = int((o["score"][0, :n] > 0).sum())
+        assert o["k_star"][0] == pos
+
+
+def test_coverage_chain_closed_form():
+    """Chain with q = 1/2: S_k = 2(1 − 2^-k), so the smallest k with S_k/S_n ≥ ρ is
+    ceil(−log2(1 − ρ(1 − 2^-n)))."""
+    import math
+    for n in (1, 2, 5, 12, 30):
+        parent = np.arange(-1, n - 1, dtype=np.int32)
+        q = np.full(n, 0.5, np.float32)
+        for rho in (0.3, 0.5, 0.75, 0.9, 0.99):
+            r = float(np.float32(rho))
+            x = 1.0 - r * (1.0 - 2.0 ** -n)
+            want = max(1, math.ceil(-math.log2(x) - 1e-12))
+            o = select1p(parent, q, np.ones(n), ("coverage", rho))
+            ties = [k + 1 for k in range(n) if (int(o["tie_bits"][0, 0]) >> k) & 1]
+            assert o["k_star"][0] == min(want, n) or o["k_star"][0] in ties
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_fixed_policy_equals_cost_policy_with_spike_table(seed):
+    """fixed-k ≡ the Eq. 10 argmax with C(j) = 1 at j = min(k, n) and 1e30 elsewhere (C(1)
+    must stay finite, Z10; S ≥ 1 makes the spike the argmax), which pins it to the
+    already-pinned cost path; the kept set is the best ancestor-closed subset of that size."""
+    rng = np.random.default_rng(2000 + seed)
+    n = int(rng.integers(1, 12))
+    parent, q = rand_tree(rng, n, dyadic=8)
+    sc = exact_scores(parent, q)
+    best, _ = best_sum_per_size(parent, sc)
+    for kf in (1, 2, 3, 5, 8, 20):
+        o = select1p(parent, q, np.ones(n), ("fixed", kf))
+        kk = min(kf, n)
+        C = np.full(n, 1e30, np.float32)
+        C[kk - 1] = 1.0
+        c = select1p(parent, q, C, None)
+        assert o["k_star"][0] == kk == c["k_star"][0]
+        assert (o["keep_bits"] == c["keep_bits"]).all()
+        kept = keep_set(o["keep_bits"][0], n)
+        assert sum(sc[v] for v in kept) == best[kk]
