@@ -65,9 +65,29 @@ def hbm_peak():
 
 
 # ------------------------------------------------------------------ clocks
+_SAMPLER = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+        nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+print("ready", flush=True)
+while True:
+    t = time.time()
+    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+    print(f"{t:.6f},{sm},{mx}," + ",".join("1" if r & b else "0" for b in bits), flush=True)
+    time.sleep(0.001)
+"""
+
+
 class ClockSampler:
-    """SM clock + throttle reasons sampled DURING the timed region: an NVML thread polling
-    every 2 ms (a K-step region can last only tens of ms), nvidia-smi -lms 100 as fallback."""
+    """SM clock + throttle reasons sampled DURING the timed region by a separate NVML process
+    (no GIL sharing with the launching thread) polling every ~1 ms; only samples whose host
+    timestamp falls inside [region start, region end] are kept.  nvidia-smi -lms 100 is the
+    fallback when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -77,78 +97,64 @@ class ClockSampler:
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.proc = None
-        self.thread = None
-        self.rows = []
-        self.active = False
+        self.kind = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
-            import threading
-            import pynvml as nv
-            nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
-            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
-                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
-            mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
-            self.stop_evt = threading.Event()
-
-            def run():
-                while not self.stop_evt.is_set():
-                    if self.active:
-                        try:
-                            sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-                            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                            self.rows.append((sm, mx, ["Active" if r & bt else "Not Active" for bt in bits]))
-                        except Exception:
-                            pass
-                    time.sleep(0.002)
-
-            self.thread = threading.Thread(target=run, daemon=True)
-            self.thread.start()
-            return
+            self.proc = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.gpu)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            if self.proc.stdout.readline().strip() == "ready":
+                self.kind = "nvml"
+                return
+            self.proc.kill()
         except Exception:
-            self.thread = None
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.kind = "smi"
         except Exception:
             self.proc = None
 
     def region(self, on):
-        """Mark the timed region (the NVML thread only records samples inside it)."""
-        self.active = on
+        """Mark the timed region by host wall clock."""
+        if on:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
 
     def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
         rows = []
-        if self.thread is not None:
-            self.active = False
-            self.stop_evt.set()
-            self.thread.join(timeout=2)
-            rows = self.rows
-        elif self.proc is not None:
-            self.proc.terminate()
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
             try:
-                out, _ = self.proc.communicate(timeout=5)
-            except Exception:
-                self.proc.kill()
-                out = ""
-            for line in out.strip().splitlines():
-                f = [x.strip() for x in line.split(",")]
-                if len(f) < 8:
-                    continue
-                try:
+                if self.kind == "nvml" and len(f) == 7:
+                    t = float(f[0])
+                    if self.t0 is not None and self.t1 is not None and not (self.t0 <= t <= self.t1):
+                        continue
+                    rows.append((float(f[1]), float(f[2]), ["Active" if x == "1" else "" for x in f[3:7]]))
+                elif self.kind == "smi" and len(f) >= 8:
                     rows.append((float(f[0]), float(f[1]), f[4:8]))
-                except ValueError:
-                    continue
+            except ValueError:
+                continue
         if not rows:
             return None
         sm = sorted(r[0] for r in rows)
         reasons = sorted({self.NAMES[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows),
                 "reasons": reasons, "samples": len(rows),
-                "source": "nvml 2 ms" if self.thread is not None else "nvidia-smi 100 ms"}
+                "source": "nvml process ~1 ms, timed region only" if self.kind == "nvml" else "nvidia-smi 100 ms"}
 
 
 # ------------------------------------------------------------------ algorithmic bytes
@@ -337,6 +343,27 @@ def mask_variant(ev, gen, torch, P, Q, n, cost, ids8, M, stream, reps):
                          "frac": ach / peak, "algorithmic_bytes_per_launch": abytes}}
 
 
+def policy_variants(ev, torch, P, Q, n, cost, ids8, M, stream, reps):
+    """NEXT-2: the same C5 sweep (select + build + union, u8 routing) cut by the score-coverage
+    rule (rho = 1 is EAGLE-3) and by a fixed k: throughput, mean k* and the
+    HBM roofline of each (the union reads k*·384 B per tree, so the cut moves the bytes)."""
+    out = {}
+    peak, _ = hbm_peak()
+    for name, pol in (("coverage_0.7", ("coverage", 0.7)), ("coverage_0.4", ("coverage", 0.4)),
+                      ("eagle3_rho_1", ("coverage", 1.0)), ("fixed_8", ("fixed", 8))):
+        call = ev.FusedCall(P, Q, cost, ids8, N_EXPERTS, n_nodes=n, policy=pol)
+        ms = time_fused(ev, torch, call, stream, reps)
+        k_sum = int(call.buffers.t["k_star"].sum())
+        abytes, _ = algorithmic_bytes(int(n.sum()), k_sum, M, 1, id_format="u8")
+        ach = abytes / (ms / 1e3) / 1e9
+        out[name] = {"value": M / (ms / 1e3), "unit": "trees/s", "kernel_ms": ms, "mean_k": k_sum / M,
+                     "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                                  "frac": ach / peak}}
+        del call
+    torch.cuda.empty_cache()
+    return out
+
+
 def router_bench(ev, gen, torch, stream):
     """A8: router logits GEMM (tcgen05) + TopK + union on the C2/C3/C4 shapes.
     Bytes = L·(T·d + E·d)·2, flops = 2·L·T·d·E with T = packed kept rows (Σ k*)."""
@@ -502,6 +529,10 @@ def run_native(args, rank, world, local_rank):
                                                        max(3, K // 2))}
         except Exception as e:  # pragma: no cover
             result["variants"] = {"mask": {"error": repr(e)}}
+        try:
+            result["policies"] = policy_variants(ev, torch, P, Q, n, cost, ids, M, stream, max(3, K // 2))
+        except Exception as e:  # pragma: no cover
+            result["policies"] = {"error": repr(e)}
     if rank == 0 and not args.no_extras:
         try:
             result["router"] = router_bench(ev, gen, torch, stream)

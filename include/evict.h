@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define EVICT_ABI_VERSION 2
+#define EVICT_ABI_VERSION 3
 #define EVICT_MAX_NODES 128   /* N ≤ 128 ⇒ W ≤ 2 mask words */
 #define EVICT_MAX_EXPERTS 256 /* Ling-flash-2.0 has 256 experts */
 #define EVICT_MAX_TOPK 16
@@ -103,6 +103,38 @@ typedef struct {
 evict_status_t evict_select(const evict_trees_t *trees, const float *cost, int32_t cost_stride,
                             int32_t *k_star, float *e_hat, float *utility, uint64_t *keep_bits,
                             int32_t *order, float *prefix_sums, uint32_t *status, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Selection policies: the same ranking and prefix
+ * sums, a different cut k*.
+ *   EVICT_POLICY_COST      Eq. 10 (the default; what evict_select does)
+ *   EVICT_POLICY_COVERAGE  k* = smallest k with S_k / S_K ≥ rho, K = n_b,
+ *                          S_k / S_K an fp32 IEEE division; the score-
+ *                          coverage ablation of PAPER.md:290–292 (§5.4),
+ *                          rho = 1 is EAGLE-3 (every node verified).
+ *                          Requires 0 < rho ≤ 1.
+ *   EVICT_POLICY_FIXED     k* = min(k_fixed, n_b), k_fixed ≥ 1.
+ * e_hat = S[k*] and utility = S[k*]/C(k*) under every policy; the cost
+ * table is still validated (it prices the reported utility).
+ * evict_select_policy / evict_select_build_union_policy take the policy
+ * (NULL = EVICT_POLICY_COST); otherwise identical to the calls without it.
+ * ------------------------------------------------------------------------- */
+typedef enum {
+    EVICT_POLICY_COST = 0,
+    EVICT_POLICY_COVERAGE = 1,
+    EVICT_POLICY_FIXED = 2
+} evict_policy_kind_t;
+
+typedef struct {
+    int32_t kind;     /* evict_policy_kind_t */
+    float rho;        /* COVERAGE */
+    int32_t k_fixed;  /* FIXED */
+} evict_policy_t;
+
+evict_status_t evict_select_policy(const evict_trees_t *trees, const float *cost, int32_t cost_stride,
+                                   const evict_policy_t *policy, int32_t *k_star, float *e_hat,
+                                   float *utility, uint64_t *keep_bits, int32_t *order,
+                                   float *prefix_sums, uint32_t *status, void *stream);
 
 /* ---------------------------------------------------------------------------
  * evict_build_verify_tree — A6 (Fig. 4(c); layout Z12).
@@ -199,6 +231,12 @@ evict_status_t evict_select_build_union(const evict_trees_t *trees, const float 
                                         int32_t cost_stride, const evict_routing_t *routing,
                                         const evict_fused_out_t *out, void *workspace,
                                         size_t workspace_bytes, void *stream);
+
+evict_status_t evict_select_build_union_policy(const evict_trees_t *trees, const float *cost,
+                                               int32_t cost_stride, const evict_policy_t *policy,
+                                               const evict_routing_t *routing,
+                                               const evict_fused_out_t *out, void *workspace,
+                                               size_t workspace_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
  * evict_router_union — A8 → A7 (Eq. 4–5; Z14, Z15).

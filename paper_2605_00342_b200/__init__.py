@@ -44,6 +44,25 @@ class _Routing(ctypes.Structure):
                 ("top_k", ctypes.c_int32), ("id_format", ctypes.c_int32), ("ids", ctypes.c_void_p)]
 
 
+class _Policy(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("rho", ctypes.c_float), ("k_fixed", ctypes.c_int32)]
+
+
+POLICY_KINDS = {"cost": 0, "coverage": 1, "fixed": 2}
+
+
+def _policy(policy):
+    """None / ("cost",) → NULL (Eq. 10); ("coverage", rho); ("fixed", k)."""
+    if policy is None or policy[0] == "cost":
+        return None
+    kind = POLICY_KINDS[policy[0]]
+    return _Policy(kind, float(policy[1]) if kind == 1 else 0.0, int(policy[1]) if kind == 2 else 0)
+
+
+def _pp(pol):
+    return ctypes.byref(pol) if pol is not None else None
+
+
 class _Router(ctypes.Structure):
     _fields_ = [("num_layers", ctypes.c_int32), ("num_experts", ctypes.c_int32),
                 ("top_k", ctypes.c_int32), ("hidden_dim", ctypes.c_int32),
@@ -77,6 +96,8 @@ def lib():
             L.evict_build_verify_tree.argtypes = [vp] * 12 + [sz, vp]
             L.evict_expert_union.argtypes = [vp] * 9
             L.evict_select_build_union.argtypes = [vp, vp, i32, vp, vp, vp, sz, vp]
+            L.evict_select_policy.argtypes = [vp, vp, i32, vp] + [vp] * 8
+            L.evict_select_build_union_policy.argtypes = [vp, vp, i32, vp, vp, vp, vp, sz, vp]
             L.evict_router_union.argtypes = [vp] * 9
             L.evict_batch_stats.argtypes = [i32, i32, i32] + [vp] * 9
             L.evict_workspace_bytes.argtypes = [i32]
@@ -84,7 +105,8 @@ def lib():
             L.evict_status_string.argtypes = [ctypes.c_int]
             L.evict_status_string.restype = ctypes.c_char_p
             for f in ("evict_select", "evict_build_verify_tree", "evict_expert_union",
-                      "evict_select_build_union", "evict_router_union", "evict_batch_stats"):
+                      "evict_select_build_union", "evict_router_union", "evict_batch_stats",
+                      "evict_select_policy", "evict_select_build_union_policy"):
                 getattr(L, f).restype = ctypes.c_int
             _lib = L
     return _lib
@@ -133,7 +155,8 @@ def new_workspace(batch, device):
 
 
 # ----------------------------------------------------------------- select (A1–A5)
-def evict_select(parent, q, cost, n_nodes=None, cost_stride=0, with_order=False, stream=None):
+def evict_select(parent, q, cost, n_nodes=None, cost_stride=0, with_order=False, policy=None,
+                 stream=None):
     B, N = parent.shape
     dev = _dev(parent)
     W = (N + 63) // 64
@@ -146,11 +169,12 @@ def evict_select(parent, q, cost, n_nodes=None, cost_stride=0, with_order=False,
         out["order"] = torch.empty((B, N), dtype=torch.int32, device=dev)
         out["prefix_sums"] = torch.empty((B, N), dtype=torch.float32, device=dev)
     tr = _trees(parent, q, n_nodes)
-    rc = lib().evict_select(ctypes.byref(tr), _p(cost), cost_stride, _p(out["k_star"]),
-                            _p(out["e_hat"]), _p(out["utility"]), _p(out["keep_bits"]),
-                            _p(out.get("order")), _p(out.get("prefix_sums")), _p(out["status"]),
-                            _stream(stream))
-    _check(rc, "evict_select")
+    pol = _policy(policy)
+    rc = lib().evict_select_policy(ctypes.byref(tr), _p(cost), cost_stride, _pp(pol), _p(out["k_star"]),
+                                   _p(out["e_hat"]), _p(out["utility"]), _p(out["keep_bits"]),
+                                   _p(out.get("order")), _p(out.get("prefix_sums")), _p(out["status"]),
+                                   _stream(stream))
+    _check(rc, "evict_select_policy")
     return out
 
 
@@ -250,7 +274,7 @@ class FusedBuffers:
 
 
 def evict_select_build_union(parent, q, cost, ids, num_experts, n_nodes=None, cost_stride=0,
-                             pos_offset=None, buffers=None, stream=None, **buf_kw):
+                             pos_offset=None, buffers=None, policy=None, stream=None, **buf_kw):
     B, N = parent.shape
     L = ids.shape[2]
     if buffers is None:
@@ -258,10 +282,11 @@ def evict_select_build_union(parent, q, cost, ids, num_experts, n_nodes=None, co
     tr = _trees(parent, q, n_nodes)
     rt = _routing(ids, num_experts)
     o = buffers.struct(pos_offset)
-    rc = lib().evict_select_build_union(ctypes.byref(tr), _p(cost), cost_stride, ctypes.byref(rt),
-                                        ctypes.byref(o), _p(buffers.workspace),
-                                        buffers.workspace.numel() * 8, _stream(stream))
-    _check(rc, "evict_select_build_union")
+    pol = _policy(policy)
+    rc = lib().evict_select_build_union_policy(ctypes.byref(tr), _p(cost), cost_stride, _pp(pol),
+                                               ctypes.byref(rt), ctypes.byref(o), _p(buffers.workspace),
+                                               buffers.workspace.numel() * 8, _stream(stream))
+    _check(rc, "evict_select_build_union_policy")
     return buffers.t
 
 
@@ -269,7 +294,7 @@ class FusedCall:
     """A pre-marshalled evict_select_build_union call (for CUDA-graph capture and timing loops)."""
 
     def __init__(self, parent, q, cost, ids, num_experts, n_nodes=None, cost_stride=0,
-                 pos_offset=None, buffers=None, **buf_kw):
+                 pos_offset=None, buffers=None, policy=None, **buf_kw):
         B, N = parent.shape
         L = ids.shape[2]
         self.keep = (parent, q, cost, ids, n_nodes, pos_offset)
@@ -281,10 +306,11 @@ class FusedCall:
         self.cs = cost_stride
         self.ws = _p(self.buffers.workspace)
         self.wsb = self.buffers.workspace.numel() * 8
-        self.fn = lib().evict_select_build_union
+        self.pol = _policy(policy)
+        self.fn = lib().evict_select_build_union_policy
 
     def __call__(self, stream=None):
-        rc = self.fn(ctypes.byref(self.tr), self.cost, self.cs, ctypes.byref(self.rt),
+        rc = self.fn(ctypes.byref(self.tr), self.cost, self.cs, _pp(self.pol), ctypes.byref(self.rt),
                      ctypes.byref(self.o), self.ws, self.wsb, _stream(stream))
         if rc:
             raise EvictError(rc, "evict_select_build_union")

@@ -91,10 +91,37 @@ size_t evict_workspace_bytes(int32_t batch)
     return 8 * (1 + ntiles);
 }
 
+static bool policy_ok(const evict_policy_t *p, evict_policy_t *out)
+{
+    *out = evict_policy_t{EVICT_POLICY_COST, 0.f, 0};
+    if (!p) return true;
+    if (p->kind == EVICT_POLICY_COST) return true;
+    if (p->kind == EVICT_POLICY_COVERAGE) {
+        if (!(p->rho > 0.f && p->rho <= 1.f)) return false;   // also rejects NaN
+    } else if (p->kind == EVICT_POLICY_FIXED) {
+        if (p->k_fixed < 1) return false;
+    } else {
+        return false;
+    }
+    *out = *p;
+    return true;
+}
+
 evict_status_t evict_select(const evict_trees_t *trees, const float *cost, int32_t cost_stride,
                             int32_t *k_star, float *e_hat, float *utility, uint64_t *keep_bits,
                             int32_t *order, float *prefix_sums, uint32_t *status, void *stream)
 {
+    return evict_select_policy(trees, cost, cost_stride, nullptr, k_star, e_hat, utility, keep_bits,
+                               order, prefix_sums, status, stream);
+}
+
+evict_status_t evict_select_policy(const evict_trees_t *trees, const float *cost, int32_t cost_stride,
+                                   const evict_policy_t *policy, int32_t *k_star, float *e_hat,
+                                   float *utility, uint64_t *keep_bits, int32_t *order,
+                                   float *prefix_sums, uint32_t *status, void *stream)
+{
+    evict_policy_t pol;
+    if (!policy_ok(policy, &pol)) return EVICT_ERR_INVALID_ARG;
     evict_status_t rc = check_trees(trees);
     if (rc) return rc;
     if (!cost || !k_star || !e_hat || !utility || !keep_bits || cost_stride < 0) return EVICT_ERR_INVALID_ARG;
@@ -103,8 +130,10 @@ evict_status_t evict_select(const evict_trees_t *trees, const float *cost, int32
     if (!dev_info().ok) return EVICT_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     if (wide(trees->max_nodes))
-        return launch_select<4>(trees, cost, cost_stride, k_star, e_hat, utility, keep_bits, order, prefix_sums, status, s);
-    return launch_select<2>(trees, cost, cost_stride, k_star, e_hat, utility, keep_bits, order, prefix_sums, status, s);
+        return launch_select<4>(trees, cost, cost_stride, pol, k_star, e_hat, utility, keep_bits, order,
+                                prefix_sums, status, s);
+    return launch_select<2>(trees, cost, cost_stride, pol, k_star, e_hat, utility, keep_bits, order,
+                            prefix_sums, status, s);
 }
 
 evict_status_t evict_build_verify_tree(const evict_trees_t *trees, const uint64_t *keep_bits,
@@ -156,6 +185,18 @@ evict_status_t evict_select_build_union(const evict_trees_t *trees, const float 
                                         const evict_fused_out_t *out, void *workspace,
                                         size_t workspace_bytes, void *stream)
 {
+    return evict_select_build_union_policy(trees, cost, cost_stride, nullptr, routing, out, workspace,
+                                           workspace_bytes, stream);
+}
+
+evict_status_t evict_select_build_union_policy(const evict_trees_t *trees, const float *cost,
+                                               int32_t cost_stride, const evict_policy_t *policy,
+                                               const evict_routing_t *routing,
+                                               const evict_fused_out_t *out, void *workspace,
+                                               size_t workspace_bytes, void *stream)
+{
+    evict_policy_t pol;
+    if (!policy_ok(policy, &pol)) return EVICT_ERR_INVALID_ARG;
     evict_status_t rc = check_trees(trees);
     if (rc) return rc;
     if (!cost || cost_stride < 0 || !out || !workspace) return EVICT_ERR_INVALID_ARG;
@@ -176,8 +217,8 @@ evict_status_t evict_select_build_union(const evict_trees_t *trees, const float 
     if (cudaMemsetAsync(workspace, 0, 8 * (1 + (size_t)ntiles), s) != cudaSuccess)
         return EVICT_ERR_CUDA;
     uint64_t *ws = (uint64_t *)workspace;
-    if (wide(trees->max_nodes)) return launch_fused<4>(trees, cost, (int)cost_stride, rt, out, ws, ntiles, s);
-    return launch_fused<2>(trees, cost, (int)cost_stride, rt, out, ws, ntiles, s);
+    if (wide(trees->max_nodes)) return launch_fused<4>(trees, cost, (int)cost_stride, pol, rt, out, ws, ntiles, s);
+    return launch_fused<2>(trees, cost, (int)cost_stride, pol, rt, out, ws, ntiles, s);
 }
 
 }  // extern "C"

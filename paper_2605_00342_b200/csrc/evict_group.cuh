@@ -241,7 +241,7 @@ __device__ __forceinline__ void g_levels(GTree<G> &t, float *sd)
 template <int G>
 __device__ __forceinline__ void g_rank_argmax(GTree<G> &t, uint8_t *rk, const float (&c)[NP], int N,
                                               int32_t *__restrict__ order_row,
-                                              float *__restrict__ prefix_row)
+                                              float *__restrict__ prefix_row, const evict_policy_t &pol)
 {
     constexpr int NMAX = GShape<G>::NMAX;
     constexpr int W = GShape<G>::W;
@@ -324,10 +324,19 @@ __device__ __forceinline__ void g_rank_argmax(GTree<G> &t, uint8_t *rk, const fl
         best = Rb[r] > best ? Rb[r] : best;
     }
     const uint32_t mx = g_max<G>(best);
+    float SK = 0.f;   // S at position n−1 (coverage policy)
+    if (pol.kind == EVICT_POLICY_COVERAGE) {
+        float sl = 0.f;
+#pragma unroll
+        for (int r = 0; r < NP; r++)
+            if (base + r == t.n - 1) sl = S[r];
+        const int own = ok && t.n >= 1 ? (t.n - 1) / NP : 0;
+        SK = __shfl_sync(kFull, sl, (threadIdx.x & 31 & ~(G - 1)) + own);
+    }
     int rfirst = NP;
 #pragma unroll
     for (int r = NP - 1; r >= 0; r--)
-        if (ok && Rb[r] == mx && base + r < t.n) rfirst = r;
+        if (ok && base + r < t.n && policy_hit(pol, base + r, t.n, Rb[r], mx, S[r], SK)) rfirst = r;
     const unsigned has = __ballot_sync(kFull, rfirst < NP);
     const unsigned gm = (G == 32) ? has : ((has >> (gidx<G>() * G)) & ((1u << G) - 1u));
     const int wl = gm ? __ffs(gm) - 1 : 0;                 // smallest k wins ties (Z3)
@@ -382,7 +391,7 @@ __device__ __forceinline__ void g_rank_argmax(GTree<G> &t, uint8_t *rk, const fl
 // written (values only).
 template <int G>
 __device__ __forceinline__ void g_select_values(GTree<G> &t, const float (&c)[NP], int N,
-                                                float *__restrict__ prefix_row)
+                                                float *__restrict__ prefix_row, const evict_policy_t &pol)
 {
     constexpr int NMAX = GShape<G>::NMAX;
     constexpr int W = GShape<G>::W;
@@ -447,10 +456,19 @@ __device__ __forceinline__ void g_select_values(GTree<G> &t, const float (&c)[NP
         best = Rb[r] > best ? Rb[r] : best;
     }
     const uint32_t mx = g_max<G>(best);
+    float SK = 0.f;   // S at position n−1 (coverage policy)
+    if (pol.kind == EVICT_POLICY_COVERAGE) {
+        float sl = 0.f;
+#pragma unroll
+        for (int r = 0; r < NP; r++)
+            if (base + r == t.n - 1) sl = S[r];
+        const int own = ok && t.n >= 1 ? (t.n - 1) / NP : 0;
+        SK = __shfl_sync(kFull, sl, (threadIdx.x & 31 & ~(G - 1)) + own);
+    }
     int rfirst = NP;
 #pragma unroll
     for (int r = NP - 1; r >= 0; r--)
-        if (ok && Rb[r] == mx && base + r < t.n) rfirst = r;
+        if (ok && base + r < t.n && policy_hit(pol, base + r, t.n, Rb[r], mx, S[r], SK)) rfirst = r;
     const unsigned has = __ballot_sync(kFull, rfirst < NP);
     const unsigned gm = (G == 32) ? has : ((has >> (gidx<G>() * G)) & ((1u << G) - 1u));
     const int wl = gm ? __ffs(gm) - 1 : 0;                 // smallest k wins ties (Z3)

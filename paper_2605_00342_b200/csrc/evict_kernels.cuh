@@ -112,7 +112,7 @@ __device__ __forceinline__ int next_tile(unsigned *ticket, int *s_tile)
 // ------------------------------------------------------------ select
 template <int NPL>
 __global__ void __launch_bounds__(kWarps * 32) k_select(evict_trees_t tr, const float *cost,
-                                                        int cost_stride, int32_t *k_star,
+                                                        int cost_stride, evict_policy_t pol, int32_t *k_star,
                                                         float *e_hat, float *utility,
                                                         uint64_t *keep_bits, int32_t *order,
                                                         float *prefix_sums, uint32_t *status)
@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_select(evict_trees_t tr, const 
     float *prow = prefix_sums ? prefix_sums + (size_t)b * N : nullptr;
     if (!t.status) {
         tree_levels<NPL, true>(t, sm);
-        tree_rank_argmax<NPL>(t, sm, c, N, orow, prow);
+        tree_rank_argmax<NPL>(t, sm, c, N, orow, prow, pol);
     } else {
         t.kstar = 0; t.ehat = 0.f; t.util = 0.f;
 #pragma unroll
@@ -334,7 +334,7 @@ __host__ __device__ inline size_t fused_smem_bytes(int L, int E, bool flags)
 // different phases the full kernel's code footprint thrashes the instruction cache.
 template <int NPL, int IDF, int KT, int EW, int CL, bool LEAN = false>
 __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, const float *cost,
-                                                       int cost_stride, evict_routing_t rt,
+                                                       int cost_stride, evict_policy_t pol, evict_routing_t rt,
                                                        evict_fused_out_t out, uint64_t *ws,
                                                        int ntiles)
 {
@@ -383,8 +383,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             grp::g_levels<G, true>(t, sd);
             int32_t *orow = (active && out.order) ? out.order + (size_t)b * N : nullptr;
             float *prow = (active && out.prefix_sums) ? out.prefix_sums + (size_t)b * N : nullptr;
-            if (!LEAN && out.order) grp::g_rank_argmax<G>(t, rk, c, N, orow, prow);   // kernel-uniform
-            else grp::g_select_values<G>(t, c, N, prow);
+            if (!LEAN && out.order) grp::g_rank_argmax<G>(t, rk, c, N, orow, prow, pol);   // kernel-uniform
+            else grp::g_select_values<G>(t, c, N, prow, pol);
             const int k = t.kstar;
             EmitRec<G> &er = rec[slot];
             if (active) {
@@ -514,7 +514,7 @@ constexpr int kSelWarps = 4;
 
 template <int G>
 __global__ void __launch_bounds__(kSelWarps * 32) k_select_g(evict_trees_t tr, const float *cost,
-                                                             int cost_stride, int32_t *k_star,
+                                                             int cost_stride, evict_policy_t pol, int32_t *k_star,
                                                              float *e_hat, float *utility,
                                                              uint64_t *keep_bits, int32_t *order,
                                                              float *prefix_sums, uint32_t *status)
@@ -538,8 +538,8 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_select_g(evict_trees_t tr, c
     grp::g_levels<G, true>(t, sd_all + slot * NMAX);
     int32_t *orow = (active && order) ? order + (size_t)b * N : nullptr;
     float *prow = (active && prefix_sums) ? prefix_sums + (size_t)b * N : nullptr;
-    if (order) grp::g_rank_argmax<G>(t, rk_all + slot * NMAX, c, N, orow, prow);   // kernel-uniform
-    else grp::g_select_values<G>(t, c, N, prow);
+    if (order) grp::g_rank_argmax<G>(t, rk_all + slot * NMAX, c, N, orow, prow, pol);   // kernel-uniform
+    else grp::g_select_values<G>(t, c, N, prow, pol);
     if (!active) return;
     if (g == 0) {
         k_star[b] = t.kstar;
@@ -622,7 +622,7 @@ struct UnionLauncher {
 
 template <int NPL, int IDF, int KT, int EW, int CL>
 struct FusedLauncher {
-    static evict_status_t run(const evict_trees_t *tr, const float *cost, int cs,
+    static evict_status_t run(const evict_trees_t *tr, const float *cost, int cs, evict_policy_t pol,
                               const evict_routing_t *rt, const evict_fused_out_t *o, uint64_t *ws,
                               int ntiles, cudaStream_t s)
     {
@@ -636,20 +636,20 @@ struct FusedLauncher {
                                                (IDF == 1 || IDF == 4) && o->union_count);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         const int blocks = persistent_blocks(kern, ntiles, dyn);
-        kern<<<blocks, kWarps * 32, dyn, s>>>(*tr, cost, cs, *rt, *o, ws, ntiles);
+        kern<<<blocks, kWarps * 32, dyn, s>>>(*tr, cost, cs, pol, *rt, *o, ws, ntiles);
         return launched();
     }
 };
 
 template <int NPL>
-evict_status_t launch_select(const evict_trees_t *tr, const float *cost, int cs, int32_t *k_star,
+evict_status_t launch_select(const evict_trees_t *tr, const float *cost, int cs, evict_policy_t pol, int32_t *k_star,
                              float *e_hat, float *utility, uint64_t *keep_bits, int32_t *order,
                              float *prefix_sums, uint32_t *status, cudaStream_t s)
 {
     if (tr->batch <= 4096) {
         // latency regime (serving batches): one warp per tree, shortest dependency chain
         const int blocks = (tr->batch + kWarps - 1) / kWarps;
-        k_select<NPL><<<blocks, kWarps * 32, 0, s>>>(*tr, cost, cs, k_star, e_hat, utility, keep_bits,
+        k_select<NPL><<<blocks, kWarps * 32, 0, s>>>(*tr, cost, cs, pol, k_star, e_hat, utility, keep_bits,
                                                        order, prefix_sums, status);
         return launched();
     }
@@ -657,7 +657,7 @@ evict_status_t launch_select(const evict_trees_t *tr, const float *cost, int cs,
     constexpr int G = NPL == 2 ? 8 : 16;
     constexpr int per_cta = kSelWarps * grp::GShape<G>::TPW;
     const int blocks = (tr->batch + per_cta - 1) / per_cta;
-    k_select_g<G><<<blocks, kSelWarps * 32, 0, s>>>(*tr, cost, cs, k_star, e_hat, utility, keep_bits,
+    k_select_g<G><<<blocks, kSelWarps * 32, 0, s>>>(*tr, cost, cs, pol, k_star, e_hat, utility, keep_bits,
                                                       order, prefix_sums, status);
     return launched();
 }
@@ -685,11 +685,11 @@ evict_status_t launch_union(const evict_trees_t *tr, const uint64_t *keep, const
 }
 
 template <int NPL>
-evict_status_t launch_fused(const evict_trees_t *tr, const float *cost, int cs,
+evict_status_t launch_fused(const evict_trees_t *tr, const float *cost, int cs, evict_policy_t pol,
                             const evict_routing_t *rt, const evict_fused_out_t *o, uint64_t *ws,
                             int ntiles, cudaStream_t s)
 {
-    return dispatch_union<NPL, FusedLauncher>(rt, tr, cost, cs, rt, o, ws, ntiles, s);
+    return dispatch_union<NPL, FusedLauncher>(rt, tr, cost, cs, pol, rt, o, ws, ntiles, s);
 }
 
 }  // namespace evict

@@ -8,8 +8,8 @@
 #include "evict.h"
 
 #define EVICT_SELECT_ARGS                                                                       \
-    const evict_trees_t *, const float *, int, int32_t *, float *, float *, uint64_t *,         \
-        int32_t *, float *, uint32_t *, cudaStream_t
+    const evict_trees_t *, const float *, int, evict_policy_t, int32_t *, float *, float *,     \
+        uint64_t *, int32_t *, float *, uint32_t *, cudaStream_t
 #define EVICT_BUILD_ARGS                                                                        \
     const evict_trees_t *, const uint64_t *, const int32_t *, int32_t *, int32_t *, int32_t *,  \
         int32_t *, int32_t *, int32_t *, uint64_t *, uint32_t *, uint64_t *, int, cudaStream_t
@@ -17,7 +17,7 @@
     const evict_trees_t *, const uint64_t *, const evict_routing_t *, int32_t *, int32_t *,     \
         uint64_t *, int64_t *, uint32_t *, cudaStream_t
 #define EVICT_FUSED_ARGS                                                                        \
-    const evict_trees_t *, const float *, int, const evict_routing_t *,                         \
+    const evict_trees_t *, const float *, int, evict_policy_t, const evict_routing_t *,         \
         const evict_fused_out_t *, uint64_t *, int, cudaStream_t
 
 namespace evict {

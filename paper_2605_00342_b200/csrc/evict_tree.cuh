@@ -219,6 +219,18 @@ __device__ __forceinline__ void tree_levels(TreeState<NPL> &t, WarpSlab<NPL> &sm
     }
 }
 
+// Selection policy cut (include/evict.h, NEXT-2): does position pos (k = pos + 1)
+// qualify?  The caller takes the smallest qualifying position.  COST: the ratio
+// bits equal the maximum (Eq. 10); COVERAGE: S_k / S_K ≥ ρ in fp32 IEEE
+// division (position n−1 always qualifies); FIXED: k = min(k_fixed, n).
+__device__ __forceinline__ bool policy_hit(const evict_policy_t &pol, int pos, int n, uint32_t rb,
+                                           uint32_t mx, float s, float SK)
+{
+    if (pol.kind == EVICT_POLICY_COVERAGE) return pos == n - 1 || __fdiv_rn(s, SK) >= pol.rho;
+    if (pol.kind == EVICT_POLICY_FIXED) return pos == (pol.k_fixed < n ? pol.k_fixed : n) - 1;
+    return rb == mx;
+}
+
 // ------------------------------------------------------------ A3–A5
 // Ranks the nodes (bitonic sort), scans S[k], divides by C(k) and takes the
 // smallest argmax.  Fills t.kstar/ehat/util/keep; optionally writes order and
@@ -227,7 +239,8 @@ template <int NPL>
 __device__ __forceinline__ void tree_rank_argmax(TreeState<NPL> &t, WarpSlab<NPL> &sm,
                                                  const float (&c)[NPL], int N,
                                                  int32_t *__restrict__ order_row,
-                                                 float *__restrict__ prefix_row)
+                                                 float *__restrict__ prefix_row,
+                                                 const evict_policy_t &pol)
 {
     constexpr int NMAX = Shape<NPL>::NMAX;
     constexpr int W = Shape<NPL>::W;
@@ -308,10 +321,18 @@ __device__ __forceinline__ void tree_rank_argmax(TreeState<NPL> &t, WarpSlab<NPL
         best = Rb[r] > best ? Rb[r] : best;
     }
     const uint32_t mx = __reduce_max_sync(kFull, best);
+    float SK = 0.f;   // S at position n−1 (coverage policy)
+    if (pol.kind == EVICT_POLICY_COVERAGE) {
+        float sl = 0.f;
+#pragma unroll
+        for (int r = 0; r < NPL; r++)
+            if (base + r == t.n - 1) sl = S[r];
+        SK = __shfl_sync(kFull, sl, (t.n - 1) / NPL);
+    }
     int rfirst = NPL;
 #pragma unroll
     for (int r = NPL - 1; r >= 0; r--)
-        if (Rb[r] == mx && base + r < t.n) rfirst = r;
+        if (base + r < t.n && policy_hit(pol, base + r, t.n, Rb[r], mx, S[r], SK)) rfirst = r;
     const unsigned has = __ballot_sync(kFull, rfirst < NPL);
     const int wl = __ffs(has) - 1;               // smallest k wins ties (Z3)
     const int rf = __shfl_sync(kFull, rfirst, wl);
@@ -323,11 +344,11 @@ __device__ __forceinline__ void tree_rank_argmax(TreeState<NPL> &t, WarpSlab<NPL
     t.util = __shfl_sync(kFull, Rk, wl);
     t.kstar = wl * NPL + rf + 1;
 
-    if (order_row != nullptr && base < N) {
+    if ((order_row != nullptr || prefix_row != nullptr) && base < N) {
 #pragma unroll
         for (int r = 0; r < NPL; r++) {
-            order_row[base + r] = (base + r < t.n) ? node[r] : -1;
-            prefix_row[base + r] = (base + r < t.n) ? S[r] : 0.f;
+            if (order_row) order_row[base + r] = (base + r < t.n) ? node[r] : -1;
+            if (prefix_row) prefix_row[base + r] = (base + r < t.n) ? S[r] : 0.f;
         }
     }
     __syncwarp();

@@ -360,3 +360,57 @@ def test_select_values_path_ties(ev, N):
                       cost_stride=N)
     res, msgs = compare_select(o, {k: x[:len(trees)] for k, x in v.items()}, n_nodes=n[:len(trees)])
     assert not msgs, msgs[:5]
+
+
+# ------------------------------------------------------------------ policies (NEXT-2)
+POLICIES = [("coverage", 0.7), ("coverage", 0.4), ("coverage", 1.0), ("fixed", 1), ("fixed", 5),
+            ("fixed", 500)]
+
+
+@pytest.mark.parametrize("policy", POLICIES)
+@pytest.mark.parametrize("B,with_order", [(300, True), (300, False), (5000, True), (5000, False)])
+def test_select_policy_vs_oracle(ev, policy, B, with_order):
+    """Score-coverage and fixed-k cuts on the same ranking: warp kernel
+    (B ≤ 4096) and grouped kernels (B > 4096, value-sort path without the order row)."""
+    rng = np.random.default_rng(B + len(policy[0]))
+    N = 60
+    P, Q, n = gen.trees(77, B, N, 6, 10)
+    n[::6] = np.maximum(1, (n[::6] * rng.uniform(0.1, 1.0, len(n[::6]))).astype(np.int32))
+    adv = adversarial(N, rng)
+    Pa, Qa, na = pad_batch(adv, N)
+    P[:len(adv)], Q[:len(adv)], n[:len(adv)] = Pa, Qa, na     # ties, zero and subnormal scores
+    cost = gen.cost_table(N)
+    g = npy(ev.evict_select(T(P), T(Q), T(cost), n_nodes=T(n), with_order=with_order, policy=policy))
+    o = oracle.select(P, Q, cost, n_nodes=n, threads=8, policy=policy)
+    res, msgs = compare_select(o, g, n_nodes=n, check_order=with_order)
+    assert not msgs, msgs[:5]
+
+
+@pytest.mark.parametrize("policy", [("coverage", 0.7), ("fixed", 6)])
+@pytest.mark.parametrize("with_order", [True, False])
+def test_fused_policy_vs_oracle(ev, policy, with_order):
+    c = gen.CONFIGS["c2"]
+    B, N, L, E, K = 333, c["N"], c["L"], c["E"], c["K"]
+    P, Q, n = gen.trees(c["seed"] + 5, B, N, c["steps"], c["topk"])
+    cost = gen.cost_table(N)
+    ids = gen.routing(c["seed"], B, N, L, E, K)
+    g = npy(ev.evict_select_build_union(T(P), T(Q), T(cost), T(ids), E, n_nodes=T(n), policy=policy,
+                                        with_bits=True, with_order=with_order))
+    o = oracle.select(P, Q, cost, n_nodes=n, threads=8, policy=policy)
+    res, msgs = compare_select(o, g, n_nodes=n, check_order=with_order)
+    assert not msgs, msgs[:5]
+    keep = g["keep_bits"].view(np.uint64)
+    assert not compare_build(oracle.build_verify_tree(P, keep, n_nodes=n),
+                             {k: v for k, v in g.items() if k != "status"})
+    assert not compare_union(oracle.expert_union(keep, ids, E, n_nodes=n, threads=8), g)
+
+
+def test_policy_rejects_bad_arguments(ev):
+    import torch
+    P = torch.full((2, 8), -1, dtype=torch.int32, device="cuda")
+    P[:, 1:] = 0
+    Q = torch.full((2, 8), 0.5, device="cuda")
+    C = torch.ones(8, device="cuda")
+    for bad in (("coverage", 0.0), ("coverage", 1.5), ("coverage", float("nan")), ("fixed", 0)):
+        with pytest.raises(ev.EvictError):
+            ev.evict_select(P, Q, C, policy=bad)
