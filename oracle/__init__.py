@@ -60,6 +60,11 @@ def lib():
             L.oracle_select_batch_policy.argtypes = ([ctypes.c_int] * 3 + [vp] * 4 + [ctypes.c_int] * 2 +
                                                      [ctypes.c_double, ctypes.c_int] + [vp] * 11)
             L.oracle_select_batch_policy.restype = None
+            L.oracle_union_curve_batch.argtypes = ([ctypes.c_int] * 3 + [vp] * 3 + [ctypes.c_int] * 4 +
+                                                   [vp] * 3)
+            L.oracle_union_curve_batch.restype = None
+            L.oracle_profile_cost.argtypes = ([ctypes.c_int] * 3 + [vp] * 3 + [ctypes.c_double] * 3 + [vp])
+            L.oracle_profile_cost.restype = None
             L.oracle_build_batch.argtypes = [ctypes.c_int] * 2 + [vp] * 11
             L.oracle_build_batch.restype = None
             L.oracle_union_batch.argtypes = [ctypes.c_int] * 3 + [vp] * 3 + [ctypes.c_int] * 4 + [vp] * 4
@@ -176,6 +181,40 @@ def expert_union(keep_bits, ids, num_experts, n_nodes=None, threads=1):
 
     _fan(run, B, threads)
     return out
+
+
+def union_curve(order, ids, num_experts, n_nodes=None, threads=1, per_layer=True):
+    """NEXT-1: prefix-union curve along the ranking.  order [B][N] (evict_select's order row),
+    ids [B][N][L][K] uint8/int32.  Returns curve [B][N], curve_layer [B][N][L], status."""
+    order = _c(order, np.int32)
+    ids = np.ascontiguousarray(ids)
+    assert ids.dtype in (np.uint8, np.int32)
+    B, N, Lyr, K = ids.shape
+    out = dict(curve=np.zeros((B, N), np.int32), status=np.zeros(B, np.uint32))
+    if per_layer:
+        out["curve_layer"] = np.zeros((B, N, Lyr), np.int32)
+    n_nodes = _c(n_nodes, np.int32)
+    L = lib()
+
+    def run(r):
+        L.oracle_union_curve_batch(r[0], r[1], N, _ptr(n_nodes), _ptr(order), _ptr(ids),
+                                   ids.dtype.itemsize, Lyr, K, num_experts, _ptr(out["curve"]),
+                                   _ptr(out.get("curve_layer")), _ptr(out["status"]))
+
+    _fan(run, B, threads)
+    return out
+
+
+def profile_cost(curve, num_layers, n_nodes=None, status=None, c0=10.47, c_union=0.0915, c_tok=0.15):
+    """Offline C(k) from measured curves (fp64): Ū(k) = mean curve(k)/L over trees with n_b ≥ k."""
+    curve = _c(curve, np.int32)
+    B, N = curve.shape
+    n_nodes = _c(n_nodes, np.int32)
+    status = _c(status, np.uint32)
+    cost = np.zeros(N, np.float64)
+    lib().oracle_profile_cost(B, N, num_layers, _ptr(n_nodes), _ptr(curve), _ptr(status), c0, c_union,
+                              c_tok, _ptr(cost))
+    return cost
 
 
 def router_topk(h_bits, wg_bits, K):

@@ -437,6 +437,93 @@ void oracle_union_batch(int b_begin, int b_end, int N, const int32_t *n_nodes,
 }
 
 /* ------------------------------------------------------------------ */
+/* NEXT-1: the prefix-union curve along the ranking and the offline cost
+ * profile built from it (Fig. 1 —
+ * activated experts grow with the number of verified tokens
+ * — C(k) is profiled offline per k).
+ *   curve[k-1]          = Σ_l |∪_{j<k} E_l(order[j])|           (k = 1..n)
+ *   curve_layer[k-1][l] = |∪_{j<k} E_l(order[j])|
+ * order = the ranking (evict_select's order row); every order[j] must be a
+ * node < n (else BAD_KEEP); ids ≥ E give BAD_EXPERT.  On error the tree's
+ * curve rows are 0.  Entries past n are 0.                              */
+uint32_t oracle_union_curve_tree(int n, const int32_t *order, const void *ids, int id_bytes,
+                                 int L, int K, int E, int32_t *curve, int32_t *curve_layer)
+{
+    unsigned char seen[128][256];
+    uint32_t st = 0;
+    if (L > 128) return ORACLE_TREE_BAD_SIZE;
+    memset(seen, 0, sizeof(seen));
+    int32_t tot = 0;
+    int32_t per[128];
+    for (int l = 0; l < L; l++) per[l] = 0;
+    for (int k = 1; k <= n; k++) {
+        int v = order[k - 1];
+        if (v < 0 || v >= n) { st |= ORACLE_TREE_BAD_KEEP; break; }
+        for (int l = 0; l < L; l++) {
+            for (int j = 0; j < K; j++) {
+                size_t idx = ((size_t)v * L + l) * K + j;
+                long e = id_bytes == 1 ? (long)((const uint8_t *)ids)[idx]
+                                       : (long)((const int32_t *)ids)[idx];
+                if (e < 0 || e >= E) { st |= ORACLE_TREE_BAD_EXPERT; continue; }
+                if (!seen[l][e]) { seen[l][e] = 1; per[l]++; tot++; }
+            }
+            if (curve_layer) curve_layer[(size_t)(k - 1) * L + l] = per[l];
+        }
+        curve[k - 1] = tot;
+    }
+    if (st) {
+        for (int k = 1; k <= n; k++) {
+            curve[k - 1] = 0;
+            if (curve_layer)
+                for (int l = 0; l < L; l++) curve_layer[(size_t)(k - 1) * L + l] = 0;
+        }
+    }
+    return st;
+}
+
+void oracle_union_curve_batch(int b_begin, int b_end, int N, const int32_t *n_nodes,
+                              const int32_t *order, const void *ids, int id_bytes, int L, int K,
+                              int E, int32_t *curve, int32_t *curve_layer, uint32_t *status)
+{
+    for (int b = b_begin; b < b_end; b++) {
+        int n = n_nodes ? n_nodes[b] : N;
+        for (int i = 0; i < N; i++) {
+            curve[(size_t)b * N + i] = 0;
+            if (curve_layer)
+                for (int l = 0; l < L; l++) curve_layer[((size_t)b * N + i) * L + l] = 0;
+        }
+        if (n < 1 || n > N) { status[b] = ORACLE_TREE_BAD_SIZE; continue; }
+        const void *tids = (const uint8_t *)ids + (size_t)b * N * L * K * id_bytes;
+        status[b] = oracle_union_curve_tree(n, order + (size_t)b * N, tids, id_bytes, L, K, E,
+                                            curve + (size_t)b * N,
+                                            curve_layer ? curve_layer + (size_t)b * N * L : NULL);
+    }
+}
+
+/* Offline cost profile from the curves (reading R2 of DESIGN.md §3 with the
+ * analytic Ū(k) = E(1 − (1 − K/E)^k) replaced by the measured mean):
+ *   Ū(k) = Σ_{b: n_b ≥ k, status_b = 0} curve_b[k-1] / (L · #{those b})
+ *   C(k) = c0 + c_union·Ū(k) + c_tok·k;  C(k) = +inf when no tree has k nodes.
+ * fp64 here.                                                            */
+void oracle_profile_cost(int B, int N, int L, const int32_t *n_nodes, const int32_t *curve,
+                         const uint32_t *status, double c0, double c_union, double c_tok,
+                         double *cost)
+{
+    for (int k = 1; k <= N; k++) {
+        double sum = 0.0;
+        long cnt = 0;
+        for (int b = 0; b < B; b++) {
+            int n = n_nodes ? n_nodes[b] : N;
+            if ((status && status[b]) || n < k) continue;
+            sum += (double)curve[(size_t)b * N + k - 1];
+            cnt++;
+        }
+        cost[k - 1] = cnt ? c0 + c_union * (sum / ((double)L * (double)cnt)) + c_tok * (double)k
+                          : INFINITY;
+    }
+}
+
+/* ------------------------------------------------------------------ */
 /* A8: router TopK (Eq. 4): E(h) = TopK(W_g h, K) on raw
  * logits (Z14), ties by expert index ascending; fp64 dot products (Z15).
  * h: d bf16 values (raw uint16 bits); Wg: [E][d] bf16.  ids_out[K] in

@@ -605,3 +605,84 @@ def test_fixed_policy_equals_cost_policy_with_spike_table(seed):
         assert (o["keep_bits"] == c["keep_bits"]).all()
         kept = keep_set(o["keep_bits"][0], n)
         assert sum(sc[v] for v in kept) == best[kk]
+
+
+# ------------------------------------------------------------ union curve (NEXT-1)
+def _curve_sets(order, ids, n):
+    """Σ_l |∪_{j<k} E_l(order[j])| by Python set unions (the definition, written out)."""
+    L = ids.shape[1]
+    seen = [set() for _ in range(L)]
+    out = []
+    for k in range(n):
+        v = int(order[k])
+        for l in range(L):
+            seen[l].update(int(e) for e in ids[v, l])
+        out.append(sum(len(s) for s in seen))
+    return out
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_union_curve_set_definition(seed):
+    rng = np.random.default_rng(3000 + seed)
+    B, N, L, E, K = 5, 16, 6, 32, 4
+    P = np.full((B, N), -1, np.int32)
+    Q = np.zeros((B, N), np.float32)
+    n = rng.integers(1, N + 1, B).astype(np.int32)
+    for b in range(B):
+        p, q = rand_tree(rng, int(n[b]), dyadic=8)
+        P[b, :n[b]], Q[b, :n[b]] = p, q
+    ids = np.stack([rng.permutation(E)[:K] for _ in range(B * N * L)]).reshape(B, N, L, K).astype(np.uint8)
+    o = oracle.select(P, Q, np.ones(N, np.float32), n_nodes=n)
+    c = oracle.union_curve(o["order"], ids, E, n_nodes=n)
+    for b in range(B):
+        want = _curve_sets(o["order"][b], ids[b], int(n[b]))
+        assert c["curve"][b, :n[b]].tolist() == want
+        assert (c["curve"][b, n[b]:] == 0).all()
+        assert (c["curve_layer"][b, :n[b]].sum(axis=1) == c["curve"][b, :n[b]]).all()
+        full = oracle.expert_union(np.array([[(1 << int(n[b])) - 1 if n[b] < 64 else ~0]], np.uint64),
+                                   ids[b:b + 1], E, n_nodes=n[b:b + 1])
+        assert c["curve"][b, n[b] - 1] == full["union_total"][0]   # prefix n = the whole tree
+
+
+def test_union_curve_identical_and_disjoint_routing():
+    """Identical routing for every node: curve(k) = L·K.  Node v on experts vK..vK+K−1
+    (disjoint): curve(k) = L·min(k·K, E)."""
+    N, L, E, K = 12, 3, 32, 4
+    P = np.arange(-1, N - 1, dtype=np.int32)[None]
+    Q = np.full((1, N), 0.5, np.float32)
+    order = oracle.select(P, Q, np.ones(N, np.float32))["order"]
+    same = np.tile(np.arange(K, dtype=np.uint8), (1, N, L, 1))
+    assert (oracle.union_curve(order, same, E)["curve"][0] == L * K).all()
+    disj = np.zeros((1, N, L, K), np.uint8)
+    for v in range(N):
+        disj[0, v, :, :] = (np.arange(K) + v * K) % E
+    got = oracle.union_curve(order, disj, E)["curve"][0]
+    assert got.tolist() == [L * min((k + 1) * K, E) for k in range(N)]
+
+
+def test_profile_cost_matches_independent_routing_closed_form():
+    """With independent uniform top-K routing, E[union of k nodes] = E(1 − (1 − K/E)^k) per
+    layer (inclusion of each expert is independent across nodes); the profiled Ū(k) must sit
+    within 4σ of it, and C(k) = c0 + c_union·Ū(k) + c_tok·k; k beyond every tree is +inf."""
+    rng = np.random.default_rng(11)
+    B, N, L, E, K = 400, 24, 8, 128, 8
+    P = np.tile(np.arange(-1, N - 1, dtype=np.int32), (B, 1))
+    Q = np.full((B, N), 0.75, np.float32)
+    n = np.full(B, N, np.int32)
+    n[:100] = 20                                  # k > 20 averaged over the other 300 trees
+    ids = np.argsort(rng.random((B, N, L, E)), axis=3)[..., :K].astype(np.uint8)
+    order = oracle.select(P, Q, np.ones(N, np.float32), n_nodes=n)["order"]
+    c = oracle.union_curve(order, ids, E, n_nodes=n)
+    cost = oracle.profile_cost(c["curve"], L, n_nodes=n, c0=1.0, c_union=0.5, c_tok=0.25)
+    for k in range(1, N + 1):
+        m = int((n >= k).sum())
+        u = E * (1 - (1 - K / E) ** k)
+        # per-layer union of k nodes: variance ≤ E·p(1−p) per layer (negatively correlated sums)
+        p = 1 - (1 - K / E) ** k
+        sd = np.sqrt(E * p * (1 - p) / (L * m))
+        ubar = (cost[k - 1] - 1.0 - 0.25 * k) / 0.5
+        assert abs(ubar - u) < 4 * sd + 1e-9, (k, ubar, u)
+    n2 = np.full(B, 10, np.int32)
+    c2 = oracle.union_curve(order, ids, E, n_nodes=n2)
+    cost2 = oracle.profile_cost(c2["curve"], L, n_nodes=n2)
+    assert np.isinf(cost2[10:]).all() and np.isfinite(cost2[:10]).all()
