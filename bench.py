@@ -364,6 +364,36 @@ def policy_variants(ev, torch, P, Q, n, cost, ids8, M, stream, reps):
     return out
 
 
+def union_curve_bench(ev, torch, P, Q, n, cost, ids8, M, stream, reps=3):
+    """NEXT-1 on the C5 sweep: the prefix-union curve of every tree along its ranking reads
+    every node's routing (N·L·K = 23 KB per tree, not k*·384 B), plus the order row in and the
+    curve out (4N B each): the roofline is HBM."""
+    sel = ev.evict_select(P, Q, cost, n_nodes=n, with_order=True)
+    order = sel["order"]
+    del sel["prefix_sums"]
+    for _ in range(2):
+        ev.evict_union_curve(order, ids8, N_EXPERTS, n_nodes=n, stream=stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps):
+        g = ev.evict_union_curve(order, ids8, N_EXPERTS, n_nodes=n, stream=stream)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    Nn = order.shape[1]
+    byt = float(n.sum()) * L_LAYERS * TOP_K + M * Nn * 4 * 2 + M * 4
+    peak, _ = hbm_peak()
+    ach = byt / (ms / 1e3) / 1e9
+    res = {"value": M / (ms / 1e3), "unit": "trees/s", "kernel_ms": ms,
+           "mean_curve_at_n": float(g["curve"].max(dim=1).values.float().mean()),
+           "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                        "algorithmic_bytes_per_launch": byt}}
+    del order, g
+    torch.cuda.empty_cache()
+    return res
+
+
 def router_bench(ev, gen, torch, stream):
     """A8: router logits GEMM (tcgen05) + TopK + union on the C2/C3/C4 shapes.
     Bytes = L·(T·d + E·d)·2, flops = 2·L·T·d·E with T = packed kept rows (Σ k*)."""
@@ -533,6 +563,10 @@ def run_native(args, rank, world, local_rank):
             result["policies"] = policy_variants(ev, torch, P, Q, n, cost, ids, M, stream, max(3, K // 2))
         except Exception as e:  # pragma: no cover
             result["policies"] = {"error": repr(e)}
+        try:
+            result["union_curve"] = union_curve_bench(ev, torch, P, Q, n, cost, ids, M, stream)
+        except Exception as e:  # pragma: no cover
+            result["union_curve"] = {"error": repr(e)}
     if rank == 0 and not args.no_extras:
         try:
             result["router"] = router_bench(ev, gen, torch, stream)

@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define EVICT_ABI_VERSION 3
+#define EVICT_ABI_VERSION 4
 #define EVICT_MAX_NODES 128   /* N ≤ 128 ⇒ W ≤ 2 mask words */
 #define EVICT_MAX_EXPERTS 256 /* Ling-flash-2.0 has 256 experts */
 #define EVICT_MAX_TOPK 16
@@ -285,6 +285,39 @@ evict_status_t evict_batch_stats(int32_t batch, int32_t max_nodes, int32_t num_l
                                  const float *e_hat, const float *utility,
                                  const int32_t *union_count, const uint32_t *status,
                                  int64_t *stats, double *dstats, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * evict_union_curve — NEXT-1: the prefix-union curve along the ranking
+ * (Fig. 1: the experts a verify pass
+ * activates grow with the verified tokens).  For k = 1..n_b:
+ *   curve[b][k-1]          = Σ_l |∪_{j<k} E_l(order[b][j])|
+ *   curve_layer[b][k-1][l] = |∪_{j<k} E_l(order[b][j])|   (NULL: not written)
+ * order: int32 [B][N], the ranking (evict_select's order row); every entry
+ * below n_b must be a node < n_b (else EVICT_TREE_BAD_KEEP).  routing as in
+ * evict_expert_union (ids: E ≤ 128; masks: E ≤ 256); an id ≥ E gives
+ * EVICT_TREE_BAD_EXPERT.  Entries past n_b, and every entry of an errored
+ * tree, are 0.  status: uint32 [B] (may be NULL).
+ * ------------------------------------------------------------------------- */
+evict_status_t evict_union_curve(const evict_trees_t *trees, const int32_t *order,
+                                 const evict_routing_t *routing, int32_t *curve,
+                                 int32_t *curve_layer, uint32_t *status, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * evict_profile_cost — NEXT-1: the offline cost table C(k) from measured
+ * curves (PAPER.md:192–194 profiles C(k) offline; reading R2 with
+ * the analytic expected union replaced by the measured one):
+ *   Ū(k) = Σ_{b: status_b = 0, n_b ≥ k} curve[b][k-1] / (L · #{those b})
+ *   cost[k-1] = c0 + c_union·Ū(k) + c_tok·k, fp64 arithmetic, stored fp32;
+ *   +inf when no tree has k nodes (an infeasible k, reading Z10).
+ * status may be NULL.  workspace: evict_profile_workspace_bytes(N) bytes,
+ * 8-byte aligned, overwritten.  The result is a valid evict_select cost table.
+ * ------------------------------------------------------------------------- */
+size_t evict_profile_workspace_bytes(int32_t max_nodes);
+evict_status_t evict_profile_cost(int32_t batch, int32_t max_nodes, int32_t num_layers,
+                                  const int32_t *n_nodes, const int32_t *curve,
+                                  const uint32_t *status, float c0, float c_union, float c_tok,
+                                  float *cost, void *workspace, size_t workspace_bytes,
+                                  void *stream);
 
 const char *evict_status_string(evict_status_t s);
 int evict_abi_version(void);

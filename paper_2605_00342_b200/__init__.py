@@ -97,6 +97,10 @@ def lib():
             L.evict_expert_union.argtypes = [vp] * 9
             L.evict_select_build_union.argtypes = [vp, vp, i32, vp, vp, vp, sz, vp]
             L.evict_select_policy.argtypes = [vp, vp, i32, vp] + [vp] * 8
+            L.evict_union_curve.argtypes = [vp] * 7
+            L.evict_profile_workspace_bytes.argtypes = [i32]
+            L.evict_profile_workspace_bytes.restype = sz
+            L.evict_profile_cost.argtypes = ([i32] * 3 + [vp] * 3 + [ctypes.c_float] * 3 + [vp, vp, sz, vp])
             L.evict_select_build_union_policy.argtypes = [vp, vp, i32, vp, vp, vp, vp, sz, vp]
             L.evict_router_union.argtypes = [vp] * 9
             L.evict_batch_stats.argtypes = [i32, i32, i32] + [vp] * 9
@@ -106,7 +110,8 @@ def lib():
             L.evict_status_string.restype = ctypes.c_char_p
             for f in ("evict_select", "evict_build_verify_tree", "evict_expert_union",
                       "evict_select_build_union", "evict_router_union", "evict_batch_stats",
-                      "evict_select_policy", "evict_select_build_union_policy"):
+                      "evict_select_policy", "evict_select_build_union_policy", "evict_union_curve",
+                      "evict_profile_cost"):
                 getattr(L, f).restype = ctypes.c_int
             _lib = L
     return _lib
@@ -315,6 +320,36 @@ class FusedCall:
         if rc:
             raise EvictError(rc, "evict_select_build_union")
         return self.buffers.t
+
+
+# ----------------------------------------------------------------- NEXT-1: union curve + profiler
+def evict_union_curve(order, ids, num_experts, n_nodes=None, per_layer=False, stream=None):
+    """Prefix-union curve along the ranking `order` ([B][N], evict_select's order row)."""
+    B, N = order.shape
+    L = ids.shape[2]
+    dev = order.device
+    out = dict(curve=torch.empty((B, N), dtype=torch.int32, device=dev),
+               status=torch.empty(B, dtype=torch.int32, device=dev))
+    if per_layer:
+        out["curve_layer"] = torch.empty((B, N, L), dtype=torch.int32, device=dev)
+    tr = _Trees(B, N, _p(n_nodes), None, None)
+    rt = _routing(ids, num_experts)
+    rc = lib().evict_union_curve(ctypes.byref(tr), _p(order), ctypes.byref(rt), _p(out["curve"]),
+                                 _p(out.get("curve_layer")), _p(out["status"]), _stream(stream))
+    _check(rc, "evict_union_curve")
+    return out
+
+
+def evict_profile_cost(curve, num_layers, n_nodes=None, status=None, c0=10.47, c_union=0.0915, c_tok=0.15,
+                       stream=None):
+    """Offline C(k) (fp32 [N]) from measured curves; a valid evict_select cost table."""
+    B, N = curve.shape
+    cost = torch.empty(N, dtype=torch.float32, device=curve.device)
+    ws = torch.empty((lib().evict_profile_workspace_bytes(N) + 7) // 8, dtype=torch.int64, device=curve.device)
+    rc = lib().evict_profile_cost(B, N, num_layers, _p(n_nodes), _p(curve), _p(status), c0, c_union, c_tok,
+                                  _p(cost), _p(ws), ws.numel() * 8, _stream(stream))
+    _check(rc, "evict_profile_cost")
+    return cost
 
 
 # ----------------------------------------------------------------- router (A8 → A7)
