@@ -394,6 +394,83 @@ def union_curve_bench(ev, torch, P, Q, n, cost, ids8, M, stream, reps=3):
     return res
 
 
+def verify_bench(ev, gen, torch, stream):
+    """NEXT-3: Eq. 3 tree sampling (and greedy T = 0) on the verify side, Qwen3 vocabulary
+    V = 151936.  Trees: the C2 generator (60 nodes), keep = Eq. 10 (evict_select), packed
+    verify tree from evict_build_verify_tree, target rows from gen/verify.py (64 distinct
+    trees; the 1024-tree batch repeats them 16× in HBM so every tree reads its own rows).
+    Algorithmic bytes per tree: sampling = the bonus row (4V) + k gathers + uniforms/links;
+    greedy = accept_len rows (4V each).  Batch 1024 moves ≥ 620 MB ≫ L2; the batch-64
+    latency flushes L2 (256 MB write) before every timed launch."""
+    import numpy as np
+    from gen import verify as gv
+    V = gv.QWEN3_VOCAB
+    B0, Nn, rep = 64, 60, 16
+    P, Q, n = gen.trees(21, B0, Nn, 6, 10)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    sel = ev.evict_select(cu(P), cu(Q), cu(gen.cost_table(Nn)), n_nodes=cu(n))
+    vt = ev.evict_build_verify_tree(cu(P), sel["keep_bits"], n_nodes=cu(n))
+    off = vt["verify_offsets"].cpu().numpy()
+    T0 = int(off[-1])
+    kept = vt["kept_index"][:T0].cpu().numpy()
+    tok = gv.draft_tokens(21, P, V, n_nodes=n)
+    rows = cu(gv.target_rows(21, P, Q, tok, np.repeat(np.arange(B0), np.diff(off)), kept, V, n_nodes=n))
+    ua, ub = gv.uniforms(21, B0 * rep, Nn)
+    B = B0 * rep
+    # 16 copies of the batch: offsets shift by T0 per copy, retrieve_index by B0·N per copy
+    offs = np.concatenate([off[:-1] + r * T0 for r in range(rep)] + [[rep * T0]]).astype(np.int32)
+    nt = vt["next_token"][:T0].repeat(rep)
+    ns = vt["next_sibling"][:T0].repeat(rep)
+    ri = torch.cat([vt["retrieve_index"][:T0] + r * B0 * Nn for r in range(rep)])
+    probs = rows.repeat(rep, 1)
+    tokb = cu(np.tile(tok, (rep, 1)))
+    args = (cu(offs), nt.contiguous(), ns.contiguous(), ri.contiguous(), tokb, probs)
+    uA, uB = cu(ua.view(np.int32)), cu(ub.view(np.int32))
+    peak, _ = hbm_peak()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    res = {"vocab": V, "trees": B, "rows": rep * T0, "probs_bytes": int(probs.numel() * 4)}
+    for mode in ("sample", "greedy"):
+        greedy = mode == "greedy"
+        call = lambda: ev.evict_verify_sample(*args, u_accept=uA, u_bonus=uB, greedy=greedy,  # noqa: E731
+                                              stream=stream)
+        for _ in range(3):
+            g = call()
+        reps = 20
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            g = call()
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        alen = g["accept_len"].double()
+        assert int((g["status"] != 0).sum()) == 0
+        rows_read = float(B) if not greedy else float(alen.sum())
+        k_sum = float(np.diff(offs).sum())
+        byt = rows_read * V * 4 + k_sum * 4 * 5 + B * (Nn * 4 + 4 * 4 + 8)
+        ach = byt / (ms / 1e3) / 1e9
+        # batch-64 latency, cold L2, through the first 64 trees
+        a64 = (args[0][:B0 + 1].contiguous(), *args[1:4], tokb[:B0].contiguous(), probs)
+        lat = []
+        for _ in range(10):
+            flush.fill_(1)
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            ev.evict_verify_sample(*a64, u_accept=uA[:B0], u_bonus=uB[:B0], greedy=greedy, stream=stream)
+            f1.record(stream)
+            f1.synchronize()
+            lat.append(f0.elapsed_time(f1) * 1e3)
+        res[mode] = {"value": B / (ms / 1e3), "unit": "trees/s", "kernel_ms": ms,
+                     "mean_accept_len": float(alen.mean()),
+                     "b64_cold_us": float(np.median(lat)),
+                     "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                                  "frac": ach / peak, "algorithmic_bytes_per_launch": byt}}
+    del probs, rows, flush
+    torch.cuda.empty_cache()
+    return res
+
+
 def router_bench(ev, gen, torch, stream):
     """A8: router logits GEMM (tcgen05) + TopK + union on the C2/C3/C4 shapes.
     Bytes = L·(T·d + E·d)·2, flops = 2·L·T·d·E with T = packed kept rows (Σ k*)."""
@@ -572,6 +649,10 @@ def run_native(args, rank, world, local_rank):
             result["router"] = router_bench(ev, gen, torch, stream)
         except Exception as e:  # pragma: no cover
             result["router"] = {"error": repr(e)}
+        try:
+            result["verify"] = verify_bench(ev, gen, torch, stream)
+        except Exception as e:  # pragma: no cover
+            result["verify"] = {"error": repr(e)}
         try:
             result["latency"] = latency_b64(ev, torch, gen)
             result["latency"].update({k.replace("n60", "n128"): v for k, v in

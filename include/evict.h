@@ -51,11 +51,12 @@
 extern "C" {
 #endif
 
-#define EVICT_ABI_VERSION 4
+#define EVICT_ABI_VERSION 5
 #define EVICT_MAX_NODES 128   /* N ≤ 128 ⇒ W ≤ 2 mask words */
 #define EVICT_MAX_EXPERTS 256 /* Ling-flash-2.0 has 256 experts */
 #define EVICT_MAX_TOPK 16
 #define EVICT_MAX_LAYERS 128
+#define EVICT_MAX_VOCAB 262144  /* target vocabulary bound of evict_verify_sample */
 
 typedef enum {
     EVICT_OK = 0,
@@ -71,6 +72,7 @@ typedef enum {
 #define EVICT_TREE_BAD_COST 0x08u   /* cost[k-1] NaN or ≤ 0 for a k ≤ n, or cost[0] = +inf */
 #define EVICT_TREE_BAD_EXPERT 0x10u /* a kept node routes to an expert id outside [0, E) */
 #define EVICT_TREE_BAD_KEEP 0x20u   /* keep set misses the root, is not ancestor-closed, or keeps a pad */
+#define EVICT_TREE_BAD_TOKEN 0x40u  /* a kept non-root node's draft token is outside [0, V) */
 
 /* A batch of draft trees (the drafter's tree rooted at x_{t+1}).
  * Nodes are numbered topologically: parent[0] = -1, 0 ≤ parent[i] < i.
@@ -318,6 +320,59 @@ evict_status_t evict_profile_cost(int32_t batch, int32_t max_nodes, int32_t num_
                                   const uint32_t *status, float c0, float c_union, float c_tok,
                                   float *cost, void *workspace, size_t workspace_bytes,
                                   void *stream);
+
+/* ---------------------------------------------------------------------------
+ * evict_verify_sample — NEXT-3: verify-side tree sampling (PAPER.md:64–72,
+ * §2.1, Eq. 3) on the packed verify tree of evict_build_verify_tree, after
+ * the target's single verify pass produced one next-token distribution per
+ * verified slot (p over the vocabulary after that node).
+ *   EVICT_VERIFY_SAMPLE (T > 0): from the root, visit the kept children c of
+ *     the current node u in slot order (next_token, then next_sibling);
+ *     accept c iff u_accept[b][c] < p_u(token(c))·2^32; on rejection remove
+ *     c's mass and renormalise p_u(w) ← p_u(w)/(1 − p_u(c)) (Eq. 3), fp32,
+ *     one IEEE division per rejected sibling in visiting order (reading V3).
+ *     When every kept child of u is rejected (or u is a leaf) the bonus
+ *     token is the inverse CDF of the residual (p_u with the rejected tokens
+ *     zeroed) at u_bonus[b]/2^32, computed EXACTLY: the smallest t with
+ *     Σ_{w≤t} r(w) > ⌊u_bonus·Σ_w r(w)/2^32⌋ in units of 2^-149 (reading V4).
+ *   EVICT_VERIFY_GREEDY (T = 0): accept the first kept child whose token is
+ *     argmax_w p_u(w) (smallest w on ties); the bonus is that argmax (V5).
+ * Inputs (DEVICE, caller-owned):
+ *   vb->verify_offsets [B+1], next_token / next_sibling / retrieve_index [T]:
+ *     evict_build_verify_tree's packed outputs (slot links local to a tree;
+ *     retrieve_index = b·N + node); vb->tokens [B·N] int32 draft token of
+ *     every node (node-indexed, gathered through retrieve_index; the root's is
+ *     unused); vb->max_nodes = N.
+ *   probs fp32 [T][row_stride]: row off_b + s is the target distribution
+ *     after slot s of tree b; entries in [0, 1]; row_stride ≥ vocab, % 4 == 0,
+ *     probs 16-byte aligned; vocab ≤ EVICT_MAX_VOCAB.
+ *   u_accept uint32 [B][N] (slot-indexed), u_bonus uint32 [B]: the uniforms
+ *     (u/2^32), required for SAMPLE, ignored for GREEDY (may be NULL).
+ * Outputs: accept_len [B] (nodes on the accepted path, root included; 0 on
+ *   error), accepted_slots [B][N] (the path's slots, -1 pad), bonus_token [B]
+ *   (-1 on error), status [B] (NULL to skip): BAD_SIZE (k_b > N), BAD_KEEP
+ *   (k_b = 0, or links not strictly increasing within [0, k_b), or a slot
+ *   with no parent), BAD_TOKEN, BAD_PROB (a gathered child probability, the
+ *   bonus row or a greedy row outside [0, 1] or NaN; or an empty residual).
+ *   Checks apply in that order; the first failing one is reported.
+ * ------------------------------------------------------------------------- */
+#define EVICT_VERIFY_SAMPLE 0
+#define EVICT_VERIFY_GREEDY 1
+
+typedef struct {
+    int32_t batch;                  /* B ≥ 1 */
+    int32_t max_nodes;              /* N, 1..128: stride of tokens rows, u_accept and accepted_slots */
+    const int32_t *verify_offsets;  /* [B+1] */
+    const int32_t *next_token;      /* [T] */
+    const int32_t *next_sibling;    /* [T] */
+    const int32_t *retrieve_index;  /* [T] */
+    const int32_t *tokens;          /* [B][N] */
+} evict_verify_batch_t;
+
+evict_status_t evict_verify_sample(const evict_verify_batch_t *vb, const float *probs, int32_t vocab,
+                                   int64_t row_stride, int32_t mode, const uint32_t *u_accept,
+                                   const uint32_t *u_bonus, int32_t *accept_len, int32_t *accepted_slots,
+                                   int32_t *bonus_token, uint32_t *status, void *stream);
 
 const char *evict_status_string(evict_status_t s);
 int evict_abi_version(void);

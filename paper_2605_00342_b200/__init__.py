@@ -103,6 +103,7 @@ def lib():
             L.evict_profile_cost.argtypes = ([i32] * 3 + [vp] * 3 + [ctypes.c_float] * 3 + [vp, vp, sz, vp])
             L.evict_select_build_union_policy.argtypes = [vp, vp, i32, vp, vp, vp, vp, sz, vp]
             L.evict_router_union.argtypes = [vp] * 9
+            L.evict_verify_sample.argtypes = [vp, vp, i32, ctypes.c_int64, i32] + [vp] * 7
             L.evict_batch_stats.argtypes = [i32, i32, i32] + [vp] * 9
             L.evict_workspace_bytes.argtypes = [i32]
             L.evict_workspace_bytes.restype = sz
@@ -111,7 +112,7 @@ def lib():
             for f in ("evict_select", "evict_build_verify_tree", "evict_expert_union",
                       "evict_select_build_union", "evict_router_union", "evict_batch_stats",
                       "evict_select_policy", "evict_select_build_union_policy", "evict_union_curve",
-                      "evict_profile_cost"):
+                      "evict_profile_cost", "evict_verify_sample"):
                 getattr(L, f).restype = ctypes.c_int
             _lib = L
     return _lib
@@ -350,6 +351,42 @@ def evict_profile_cost(curve, num_layers, n_nodes=None, status=None, c0=10.47, c
                                   _p(cost), _p(ws), ws.numel() * 8, _stream(stream))
     _check(rc, "evict_profile_cost")
     return cost
+
+
+# ----------------------------------------------------------------- verify sampling (NEXT-3)
+VERIFY_SAMPLE, VERIFY_GREEDY = 0, 1
+TREE_BAD_TOKEN = 0x40
+
+
+class _VerifyBatch(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("max_nodes", ctypes.c_int32), ("verify_offsets", ctypes.c_void_p),
+                ("next_token", ctypes.c_void_p), ("next_sibling", ctypes.c_void_p),
+                ("retrieve_index", ctypes.c_void_p), ("tokens", ctypes.c_void_p)]
+
+
+def evict_verify_sample(verify_offsets, next_token, next_sibling, retrieve_index, tokens, probs,
+                        u_accept=None, u_bonus=None, greedy=False, vocab=None, stream=None, out=None):
+    """Eq. 3 tree sampling (or greedy T = 0) on the packed verify tree.
+    tokens: int32 [B][N] node-indexed draft tokens; probs: fp32 [T][stride] target rows;
+    u_accept: uint32-as-int32 [B][N]; u_bonus: [B].  Returns dict of CUDA tensors."""
+    B, N = tokens.shape
+    for t in (verify_offsets, next_token, next_sibling, retrieve_index, tokens):
+        assert t.is_cuda and t.dtype == torch.int32 and t.is_contiguous()
+    assert probs.dtype == torch.float32 and probs.dim() == 2 and probs.stride(1) == 1
+    V = probs.shape[1] if vocab is None else int(vocab)
+    dev = tokens.device
+    if out is None:
+        out = dict(accept_len=torch.empty(B, dtype=torch.int32, device=dev),
+                   accepted_slots=torch.empty((B, N), dtype=torch.int32, device=dev),
+                   bonus_token=torch.empty(B, dtype=torch.int32, device=dev),
+                   status=torch.empty(B, dtype=torch.int32, device=dev))
+    vb = _VerifyBatch(B, N, _p(verify_offsets), _p(next_token), _p(next_sibling), _p(retrieve_index), _p(tokens))
+    rc = lib().evict_verify_sample(ctypes.byref(vb), _p(probs), V, probs.stride(0),
+                                   VERIFY_GREEDY if greedy else VERIFY_SAMPLE, _p(u_accept), _p(u_bonus),
+                                   _p(out["accept_len"]), _p(out["accepted_slots"]), _p(out["bonus_token"]),
+                                   _p(out["status"]), _stream(stream))
+    _check(rc, "evict_verify_sample")
+    return out
 
 
 # ----------------------------------------------------------------- router (A8 → A7)

@@ -1,0 +1,165 @@
+"""GPU parity of evict_verify_sample (Eq. 3 tree sampling) against the
+oracle (oracle/verify.py): bit-exact accepted paths, bonus tokens and statuses."""
+import numpy as np
+import pytest
+
+import gen
+from gen import verify as gv
+from oracle import verify as ov
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(seed, B, N, V, stride=None, keep="oracle"):
+    """Trees, the oracle's keep set (Eq. 10), packed target rows in the oracle's verify layout."""
+    import oracle
+    P, Q, n = gen.trees(seed, B, N, 6, 10)
+    if keep == "oracle":
+        keep_bits = oracle.select(P, Q, gen.cost_table(N), n_nodes=n)["keep_bits"]
+    else:   # every node kept (EAGLE-3, rho = 1)
+        keep_bits = np.zeros((B, (N + 63) // 64), np.uint64)
+        for b in range(B):
+            for i in range(int(n[b])):
+                keep_bits[b, i // 64] |= np.uint64(1 << (i % 64))
+    ob = oracle.build_verify_tree(P, keep_bits, n_nodes=n)
+    off = ob["verify_offsets"]
+    T = int(off[-1])
+    row_tree = np.repeat(np.arange(B), np.diff(off))
+    row_node = ob["kept_index"][:T]
+    tok = gv.draft_tokens(seed, P, V, n_nodes=n)
+    rows = gv.target_rows(seed, P, Q, tok, row_tree, row_node, V, n_nodes=n)
+    stride = stride or V
+    probs = np.zeros((T, stride), np.float32)
+    probs[:, :V] = rows
+    ua, ub = gv.uniforms(seed, B, N)
+    return P, Q, n, keep_bits, off, tok, probs, ua, ub
+
+
+def _gpu(P, n, keep_bits, tok, probs, ua, ub, V, greedy=False, mutate=None):
+    import torch
+    import paper_2605_00342_b200 as ev
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    vt = ev.evict_build_verify_tree(cu(P), cu(keep_bits.view(np.int64)), n_nodes=cu(n))
+    args = dict(verify_offsets=vt["verify_offsets"], next_token=vt["next_token"],
+                next_sibling=vt["next_sibling"], retrieve_index=vt["retrieve_index"])
+    if mutate:
+        mutate(args)
+    out = ev.evict_verify_sample(args["verify_offsets"], args["next_token"], args["next_sibling"],
+                                 args["retrieve_index"], cu(tok), cu(probs),
+                                 u_accept=cu(ua.view(np.int32)), u_bonus=cu(ub.view(np.int32)),
+                                 greedy=greedy, vocab=V)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def _compare(o, g):
+    for key in ("status", "accept_len", "accepted_slots", "bonus_token"):
+        a, b = o[key].astype(np.int64), g[key].astype(np.int64)
+        if key == "status":
+            b = b & 0xFFFFFFFF
+        bad = np.flatnonzero((a != b).reshape(len(a), -1).any(axis=1))
+        assert bad.size == 0, (key, bad[:5], a[bad[:3]], b[bad[:3]])
+
+
+@pytest.mark.parametrize("V,stride,greedy,keep", [
+    (1000, None, False, "oracle"),
+    (4099, 4100, False, "oracle"),     # ragged vocabulary tail, padded row stride
+    (4099, 4100, True, "oracle"),
+    (2048, None, False, "all"),        # every node kept: deep walks, many siblings
+    (2048, None, True, "all"),
+])
+def test_parity_small_vocab(V, stride, greedy, keep):
+    P, Q, n, kb, off, tok, probs, ua, ub = _case(11, 64, 60, V, stride, keep)
+    mode = ov.GREEDY if greedy else ov.SAMPLE
+    o = ov.verify_sample(P, kb, tok, probs[:, :V], ua, ub, mode=mode, n_nodes=n, verify_offsets=off)
+    g = _gpu(P, n, kb, tok, probs, ua, ub, V, greedy)
+    assert (o["status"] == 0).all()
+    _compare(o, g)
+    if keep == "all" and not greedy:
+        assert o["accept_len"].max() >= 3     # the walks really descend
+
+
+@pytest.mark.parametrize("greedy", [False, True])
+def test_parity_qwen3_vocab(greedy):
+    """Full Qwen3 vocabulary (151936), the bench's launch configuration, 8 trees."""
+    V = gv.QWEN3_VOCAB
+    P, Q, n, kb, off, tok, probs, ua, ub = _case(12, 8, 60, V)
+    mode = ov.GREEDY if greedy else ov.SAMPLE
+    o = ov.verify_sample(P, kb, tok, probs, ua, ub, mode=mode, n_nodes=n, verify_offsets=off)
+    g = _gpu(P, n, kb, tok, probs, ua, ub, V, greedy)
+    _compare(o, g)
+
+
+def test_parity_uniform_extremes_and_root_only():
+    """u = 0 (accept the first child with mass) / u = 2^32-1 (reject all, bonus at the last
+    token with residual mass) and root-only keep sets (bonus from the root row)."""
+    V = 3000
+    P, Q, n, kb, off, tok, probs, ua, ub = _case(13, 32, 60, V, keep="all")
+    for fill in (0, 0xFFFFFFFF):
+        ua2 = np.full_like(ua, fill)
+        ub2 = np.full_like(ub, fill)
+        o = ov.verify_sample(P, kb, tok, probs, ua2, ub2, n_nodes=n, verify_offsets=off)
+        g = _gpu(P, n, kb, tok, probs, ua2, ub2, V)
+        _compare(o, g)
+    kb1 = np.zeros_like(kb)
+    kb1[:, 0] = 1
+    off1 = np.arange(33, dtype=np.int32)
+    probs1 = probs[off[:-1]]                  # the root rows
+    o = ov.verify_sample(P, kb1, tok, probs1, ua, ub, n_nodes=n, verify_offsets=off1)
+    g = _gpu(P, n, kb1, tok, probs1, ua, ub, V)
+    _compare(o, g)
+    assert (g["accept_len"] == 1).all()
+
+
+def test_parity_duplicate_sibling_tokens_and_subnormals():
+    """Duplicated sibling tokens (the second copy has no mass after a rejection, Eq. 3) and
+    rows of subnormal masses (exact fixed-point CDF)."""
+    V = 600
+    P, Q, n, kb, off, tok, probs, ua, ub = _case(14, 48, 60, V, keep="all")
+    rng = np.random.default_rng(1)
+    tok = tok.copy()
+    for b in range(48):                       # give some nodes their previous sibling's token
+        for i in range(2, int(n[b])):
+            if P[b, i] == P[b, i - 1] and rng.random() < 0.3:
+                tok[b, i] = tok[b, i - 1]
+    probs = probs.copy()
+    sub = rng.random(probs.shape) < 0.2
+    probs[sub] = (rng.integers(1, 1 << 20, size=sub.sum()) * 2.0 ** -149).astype(np.float32)
+    o = ov.verify_sample(P, kb, tok, probs, ua, ub, n_nodes=n, verify_offsets=off)
+    g = _gpu(P, n, kb, tok, probs, ua, ub, V)
+    _compare(o, g)
+
+
+def test_status_bad_token_and_prob():
+    V = 800
+    P, Q, n, kb, off, tok, probs, ua, ub = _case(15, 16, 60, V, keep="all")
+    tok = tok.copy()
+    tok[3, 5] = V + 7                        # a kept node's token out of range
+    probs = probs.copy()
+    probs[off[6] + 0, 17] = np.nan           # tree 6's root row (bonus row when root-only path)
+    probs[off[9] + 0, :] = 0                 # tree 9: empty root row (children masses 0)
+    o = ov.verify_sample(P, kb, tok, probs, ua, ub, n_nodes=n, verify_offsets=off)
+    g = _gpu(P, n, kb, tok, probs, ua, ub, V)
+    assert o["status"][3] == ov.TREE_BAD_TOKEN
+    assert o["status"][9] == ov.TREE_BAD_PROB
+    _compare(o, g)
+    for greedy in (True,):
+        o = ov.verify_sample(P, kb, tok, probs, ua, ub, mode=ov.GREEDY, n_nodes=n, verify_offsets=off)
+        g = _gpu(P, n, kb, tok, probs, ua, ub, V, greedy)
+        _compare(o, g)
+
+
+def test_bad_links_flag_keep():
+    import torch
+    V = 256
+    P, Q, n, kb, off, tok, probs, ua, ub = _case(16, 4, 60, V, keep="all")
+
+    def loop(args):
+        nt = args["next_sibling"].clone()
+        nt[int(off[1]) + 2] = 1              # a backwards sibling link in tree 1
+        args["next_sibling"] = nt
+
+    g = _gpu(P, n, kb, tok, probs, ua, ub, V, mutate=loop)
+    assert int(g["status"][1]) & 0xFFFFFFFF == ov.TREE_BAD_KEEP and g["accept_len"][1] == 0
+    assert (g["status"][[0, 2, 3]] == 0).all()
+    assert torch.cuda.is_available()
