@@ -358,6 +358,8 @@ evict_status_t evict_profile_cost(int32_t batch, int32_t max_nodes, int32_t num_
  * ------------------------------------------------------------------------- */
 #define EVICT_VERIFY_SAMPLE 0
 #define EVICT_VERIFY_GREEDY 1
+#define EVICT_VERIFY_EXACT 0x10  /* OR into SAMPLE: skip the certified fp64 fast path of the bonus and
+                                    always run the fixed-point one (same results; a testing aid) */
 
 typedef struct {
     int32_t batch;                  /* B ≥ 1 */

@@ -354,7 +354,7 @@ def evict_profile_cost(curve, num_layers, n_nodes=None, status=None, c0=10.47, c
 
 
 # ----------------------------------------------------------------- verify sampling (NEXT-3)
-VERIFY_SAMPLE, VERIFY_GREEDY = 0, 1
+VERIFY_SAMPLE, VERIFY_GREEDY, VERIFY_EXACT = 0, 1, 0x10
 TREE_BAD_TOKEN = 0x40
 
 
@@ -365,10 +365,11 @@ class _VerifyBatch(ctypes.Structure):
 
 
 def evict_verify_sample(verify_offsets, next_token, next_sibling, retrieve_index, tokens, probs,
-                        u_accept=None, u_bonus=None, greedy=False, vocab=None, stream=None, out=None):
+                        u_accept=None, u_bonus=None, greedy=False, vocab=None, exact=False, stream=None, out=None):
     """Eq. 3 tree sampling (or greedy T = 0) on the packed verify tree.
     tokens: int32 [B][N] node-indexed draft tokens; probs: fp32 [T][stride] target rows;
-    u_accept: uint32-as-int32 [B][N]; u_bonus: [B].  Returns dict of CUDA tensors."""
+    u_accept: uint32-as-int32 [B][N]; u_bonus: [B].  exact: force the fixed-point bonus path.
+    Returns dict of CUDA tensors."""
     B, N = tokens.shape
     for t in (verify_offsets, next_token, next_sibling, retrieve_index, tokens):
         assert t.is_cuda and t.dtype == torch.int32 and t.is_contiguous()
@@ -382,7 +383,8 @@ def evict_verify_sample(verify_offsets, next_token, next_sibling, retrieve_index
                    status=torch.empty(B, dtype=torch.int32, device=dev))
     vb = _VerifyBatch(B, N, _p(verify_offsets), _p(next_token), _p(next_sibling), _p(retrieve_index), _p(tokens))
     rc = lib().evict_verify_sample(ctypes.byref(vb), _p(probs), V, probs.stride(0),
-                                   VERIFY_GREEDY if greedy else VERIFY_SAMPLE, _p(u_accept), _p(u_bonus),
+                                   (VERIFY_GREEDY if greedy else VERIFY_SAMPLE) | (VERIFY_EXACT if exact else 0),
+                                   _p(u_accept), _p(u_bonus),
                                    _p(out["accept_len"]), _p(out["accepted_slots"]), _p(out["bonus_token"]),
                                    _p(out["status"]), _stream(stream))
     _check(rc, "evict_verify_sample")

@@ -35,7 +35,7 @@ def _case(seed, B, N, V, stride=None, keep="oracle"):
     return P, Q, n, keep_bits, off, tok, probs, ua, ub
 
 
-def _gpu(P, n, keep_bits, tok, probs, ua, ub, V, greedy=False, mutate=None):
+def _gpu(P, n, keep_bits, tok, probs, ua, ub, V, greedy=False, mutate=None, exact=False):
     import torch
     import paper_2605_00342_b200 as ev
     cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
@@ -47,7 +47,7 @@ def _gpu(P, n, keep_bits, tok, probs, ua, ub, V, greedy=False, mutate=None):
     out = ev.evict_verify_sample(args["verify_offsets"], args["next_token"], args["next_sibling"],
                                  args["retrieve_index"], cu(tok), cu(probs),
                                  u_accept=cu(ua.view(np.int32)), u_bonus=cu(ub.view(np.int32)),
-                                 greedy=greedy, vocab=V)
+                                 greedy=greedy, vocab=V, exact=exact)
     torch.cuda.synchronize()
     return {k: v.cpu().numpy() for k, v in out.items()}
 
@@ -63,6 +63,7 @@ def _compare(o, g):
 
 @pytest.mark.parametrize("V,stride,greedy,keep", [
     (1000, None, False, "oracle"),
+    (1000, None, "exact", "oracle"),   # the fixed-point bonus path forced for every tree
     (4099, 4100, False, "oracle"),     # ragged vocabulary tail, padded row stride
     (4099, 4100, True, "oracle"),
     (2048, None, False, "all"),        # every node kept: deep walks, many siblings
@@ -70,23 +71,27 @@ def _compare(o, g):
 ])
 def test_parity_small_vocab(V, stride, greedy, keep):
     P, Q, n, kb, off, tok, probs, ua, ub = _case(11, 64, 60, V, stride, keep)
+    exact = greedy == "exact"
+    greedy = greedy is True
     mode = ov.GREEDY if greedy else ov.SAMPLE
     o = ov.verify_sample(P, kb, tok, probs[:, :V], ua, ub, mode=mode, n_nodes=n, verify_offsets=off)
-    g = _gpu(P, n, kb, tok, probs, ua, ub, V, greedy)
+    g = _gpu(P, n, kb, tok, probs, ua, ub, V, greedy, exact=exact)
     assert (o["status"] == 0).all()
     _compare(o, g)
     if keep == "all" and not greedy:
         assert o["accept_len"].max() >= 3     # the walks really descend
 
 
-@pytest.mark.parametrize("greedy", [False, True])
+@pytest.mark.parametrize("greedy", [False, True, "exact"])
 def test_parity_qwen3_vocab(greedy):
     """Full Qwen3 vocabulary (151936), the bench's launch configuration, 8 trees."""
     V = gv.QWEN3_VOCAB
     P, Q, n, kb, off, tok, probs, ua, ub = _case(12, 8, 60, V)
+    exact = greedy == "exact"
+    greedy = greedy is True
     mode = ov.GREEDY if greedy else ov.SAMPLE
     o = ov.verify_sample(P, kb, tok, probs, ua, ub, mode=mode, n_nodes=n, verify_offsets=off)
-    g = _gpu(P, n, kb, tok, probs, ua, ub, V, greedy)
+    g = _gpu(P, n, kb, tok, probs, ua, ub, V, greedy, exact=exact)
     _compare(o, g)
 
 
@@ -163,3 +168,40 @@ def test_bad_links_flag_keep():
     assert int(g["status"][1]) & 0xFFFFFFFF == ov.TREE_BAD_KEEP and g["accept_len"][1] == 0
     assert (g["status"][[0, 2, 3]] == 0).all()
     assert torch.cuda.is_available()
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_parity_threshold_on_a_cdf_boundary(exact):
+    """Draws that land exactly on a CDF step (dyadic rows, u = 1/4, 1/2, 3/4, …): the fp64 fast
+    path cannot certify them and must hand over to the fixed-point path; the answer is the
+    smallest t whose CDF exceeds u (oracle), i.e. the token after the step."""
+    V, B, N = 64, 40, 4
+    rng = np.random.default_rng(3)
+    P = np.tile(np.array([-1, 0, 0, 1], np.int32), (B, 1))
+    kb = np.ones((B, 1), np.uint64)                     # root only: the bonus comes from row 0
+    tok = np.tile(np.array([0, 1, 2, 3], np.int32), (B, 1))
+    probs = np.zeros((B, V), np.float32)
+    for b in range(B):
+        idx = rng.choice(V, size=4, replace=False)
+        probs[b, idx] = [0.25, 0.25, 0.125, 0.375]
+    ub = np.array([(1 << 30) * (b % 4) + (b >= 20) for b in range(B)], np.uint32)   # on / just past steps
+    ua = np.zeros((B, N), np.uint32)
+    off = np.arange(B + 1, dtype=np.int32)
+    n = np.full(B, N, np.int32)
+    o = ov.verify_sample(P, kb, tok, probs, ua, ub, n_nodes=n, verify_offsets=off)
+    g = _gpu(P, n, kb, tok, probs, ua, ub, V, exact=exact)
+    _compare(o, g)
+
+
+@pytest.mark.parametrize("B", [150, 300, 600, 1200, 2400])
+@pytest.mark.parametrize("greedy", [False, True])
+def test_parity_cluster_sizes(B, greedy):
+    """Batch sizes that select 4-, 2- and 1-CTA clusters per tree for sampling and 1 for greedy
+    (the launch splits a tree's row over a thread-block cluster until the grid covers 16·SMs
+    CTAs for sampling, 4·SMs for greedy); batches ≤ 64 elsewhere use 8."""
+    V = 300
+    P, Q, n, kb, off, tok, probs, ua, ub = _case(17, B, 60, V, keep="all")
+    mode = ov.GREEDY if greedy else ov.SAMPLE
+    o = ov.verify_sample(P, kb, tok, probs, ua, ub, mode=mode, n_nodes=n, verify_offsets=off)
+    g = _gpu(P, n, kb, tok, probs, ua, ub, V, greedy)
+    _compare(o, g)
