@@ -471,6 +471,66 @@ def verify_bench(ev, gen, torch, stream):
     return res
 
 
+def dispatch_bench(ev, gen, torch):
+    """NEXT-4: one decoding step's selection → verify hand-off.  device: ONE graph launch
+    [captured fused EVICT step on a batch of 64 C2 trees] → k_dispatch → SWITCH over 10 verify
+    bodies (each a stand-in memset).  host (the paper's dispatch): replay the
+    captured EVICT step, read verify_offsets[B] to the host (sync), replay the chosen body.
+    µs per step, wall clock over 200 steps after warm-up, stream-synchronised at the end."""
+    import time
+    import numpy as np
+    B, N, L, E, K = 64, 60, 48, 128, 8
+    P, Q, n = gen.trees(2, B, N, 6, 10)
+    ids = gen.routing(2, B, N, L, E, K)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    s = torch.cuda.Stream()
+    lengths = [64, 128, 256, 384, 512, 640, 768, 1024, 2048, 3840]
+    marker = torch.zeros(1, dtype=torch.int32, device="cuda")
+    chosen = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+    def cap(fn):
+        g = torch.cuda.CUDAGraph(keep_graph=True)
+        with torch.cuda.graph(g, stream=s):
+            fn()
+        g.instantiate()
+        return g
+
+    with torch.cuda.stream(s):
+        call = ev.FusedCall(cu(P), cu(Q), cu(gen.cost_table(N)), cu(ids), E, n_nodes=cu(n))
+        call(s)
+        pre = cap(lambda: call(s))
+        rows = call.buffers.t["verify_offsets"][B:]
+        bodies = [cap(lambda i=i: marker.fill_(i)) for i in range(len(lengths))]
+    d = ev.VerifyDispatch(lengths, bodies, rows, chosen, pre=pre)
+    R = 200
+    for _ in range(20):
+        d.launch(s)
+    s.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(R):
+        d.launch(s)
+    s.synchronize()
+    dev_us = (time.perf_counter() - t0) / R * 1e6
+    with torch.cuda.stream(s):
+        for _ in range(20):
+            pre.replay()
+            T = int(rows.item())
+            bodies[next(i for i, x in enumerate(lengths) if x >= T)].replay()
+        s.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(R):
+            pre.replay()
+            T = int(rows.item())
+            bodies[next(i for i, x in enumerate(lengths) if x >= T)].replay()
+        s.synchronize()
+    host_us = (time.perf_counter() - t0) / R * 1e6
+    res = {"batch": B, "verify_rows": int(rows.item()), "body": int(chosen.item()),
+           "device_dispatch_us_per_step": dev_us, "host_dispatch_us_per_step": host_us,
+           "timing": "host wall clock over 200 back-to-back steps (device: graph launches, no sync per step)"}
+    d.close()
+    return res
+
+
 def router_bench(ev, gen, torch, stream):
     """A8: router logits GEMM (tcgen05) + TopK + union on the C2/C3/C4 shapes.
     Bytes = L·(T·d + E·d)·2, flops = 2·L·T·d·E with T = packed kept rows (Σ k*)."""
@@ -649,6 +709,10 @@ def run_native(args, rank, world, local_rank):
             result["router"] = router_bench(ev, gen, torch, stream)
         except Exception as e:  # pragma: no cover
             result["router"] = {"error": repr(e)}
+        try:
+            result["dispatch"] = dispatch_bench(ev, gen, torch)
+        except Exception as e:  # pragma: no cover
+            result["dispatch"] = {"error": repr(e)}
         try:
             result["verify"] = verify_bench(ev, gen, torch, stream)
         except Exception as e:  # pragma: no cover

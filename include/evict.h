@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define EVICT_ABI_VERSION 5
+#define EVICT_ABI_VERSION 6
 #define EVICT_MAX_NODES 128   /* N ≤ 128 ⇒ W ≤ 2 mask words */
 #define EVICT_MAX_EXPERTS 256 /* Ling-flash-2.0 has 256 experts */
 #define EVICT_MAX_TOPK 16
@@ -296,7 +296,7 @@ evict_status_t evict_batch_stats(int32_t batch, int32_t max_nodes, int32_t num_l
  *   curve_layer[b][k-1][l] = |∪_{j<k} E_l(order[b][j])|   (NULL: not written)
  * order: int32 [B][N], the ranking (evict_select's order row); every entry
  * below n_b must be a node < n_b (else EVICT_TREE_BAD_KEEP).  routing as in
- * evict_expert_union (ids: E ≤ 128; masks: E ≤ 256); an id ≥ E gives
+ * evict_expert_union (ids and masks: E ≤ 256); an id ≥ E gives
  * EVICT_TREE_BAD_EXPERT.  Entries past n_b, and every entry of an errored
  * tree, are 0.  status: uint32 [B] (may be NULL).
  * ------------------------------------------------------------------------- */
@@ -375,6 +375,39 @@ evict_status_t evict_verify_sample(const evict_verify_batch_t *vb, const float *
                                    int64_t row_stride, int32_t mode, const uint32_t *u_accept,
                                    const uint32_t *u_bonus, int32_t *accept_len, int32_t *accepted_slots,
                                    int32_t *bonus_token, uint32_t *status, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * On-device verify-graph dispatch — NEXT-4 (one verify
+ * graph is pre-captured per verification length and the one matching the
+ * selected length is dispatched; done on the host that needs k* on the host,
+ * a device→host sync per step).  evict_dispatch_create builds and
+ * instantiates ONE CUDA graph
+ *     [pre_graph] → k_dispatch → SWITCH { body_graphs[0] | … | [n−1] }
+ * k_dispatch reads T = *rows on the device at launch time (e.g.
+ * verify_offsets + B: the packed verify row count the step produced), takes
+ * i = the smallest index with lengths[i] ≥ T and sets the switch to it (no
+ * body runs when T > lengths[n−1]); *chosen (device int32, may be NULL)
+ * receives i or −1.  The selection never leaves the device.
+ *   n_bodies   1..EVICT_DISPATCH_MAX
+ *   lengths    HOST int32 [n_bodies], strictly ascending, ≥ 0
+ *   body_graphs HOST array of cudaGraph_t (the caller's captured verify
+ *              graphs; CLONED into the switch bodies, the caller keeps
+ *              ownership); each may hold kernel, memset, memcpy, empty and
+ *              child-graph nodes (CUDA's rule for conditional bodies)
+ *   pre_graph  cudaGraph_t or NULL, cloned, runs before the selection
+ *   rows, chosen: DEVICE pointers baked into the graph (must outlive it)
+ * The handle is a host object owned by the caller: evict_dispatch_destroy.
+ * evict_dispatch_launch = cudaGraphLaunch on `stream`.  Errors: INVALID_ARG
+ * (bad arguments), UNSUPPORTED (no sm_100 device), CUDA (graph API error).
+ * ------------------------------------------------------------------------- */
+#define EVICT_DISPATCH_MAX 32
+typedef struct evict_dispatch_s *evict_dispatch_t;
+
+evict_status_t evict_dispatch_create(int32_t n_bodies, const int32_t *lengths, void *const *body_graphs,
+                                     void *pre_graph, const int32_t *rows, int32_t *chosen,
+                                     evict_dispatch_t *out);
+evict_status_t evict_dispatch_launch(evict_dispatch_t d, void *stream);
+void evict_dispatch_destroy(evict_dispatch_t d);
 
 const char *evict_status_string(evict_status_t s);
 int evict_abi_version(void);

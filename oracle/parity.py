@@ -115,3 +115,21 @@ def compare_union(o, g, with_bits=True):
     if "status" in g and not (np.asarray(o["status"]) == np.asarray(g["status"]).astype(np.uint32)).all():
         msgs.append("union status differs")
     return msgs
+
+
+def downstream_keep(o, g, n_nodes=None):
+    """Keep sets for the downstream (build / union) comparisons, taken from the ORACLE: its own
+    keep bits, except for trees that compare_select classed as a tie (the GPU's k* differs from
+    the oracle's but lies in the oracle's near-tie set, rule 3), which use the oracle's ranking
+    prefix of the GPU's length — "the oracle evaluated at the GPU's k*".  No node set is taken
+    from the GPU."""
+    B, N = o["order"].shape
+    keep = np.array(o["keep_bits"], dtype=np.uint64, copy=True)
+    kg = np.asarray(g["k_star"])
+    for b in range(B):
+        if o["status"][b] or int(kg[b]) == int(o["k_star"][b]) or int(kg[b]) < 1:
+            continue
+        keep[b] = 0
+        for v in o["order"][b, :int(kg[b])]:
+            keep[b, v // 64] |= np.uint64(1 << int(v % 64))
+    return keep

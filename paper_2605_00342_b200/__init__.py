@@ -104,6 +104,10 @@ def lib():
             L.evict_select_build_union_policy.argtypes = [vp, vp, i32, vp, vp, vp, vp, sz, vp]
             L.evict_router_union.argtypes = [vp] * 9
             L.evict_verify_sample.argtypes = [vp, vp, i32, ctypes.c_int64, i32] + [vp] * 7
+            L.evict_dispatch_create.argtypes = [i32, vp, vp, vp, vp, vp, vp]
+            L.evict_dispatch_launch.argtypes = [vp, vp]
+            L.evict_dispatch_destroy.argtypes = [vp]
+            L.evict_dispatch_destroy.restype = None
             L.evict_batch_stats.argtypes = [i32, i32, i32] + [vp] * 9
             L.evict_workspace_bytes.argtypes = [i32]
             L.evict_workspace_bytes.restype = sz
@@ -112,7 +116,8 @@ def lib():
             for f in ("evict_select", "evict_build_verify_tree", "evict_expert_union",
                       "evict_select_build_union", "evict_router_union", "evict_batch_stats",
                       "evict_select_policy", "evict_select_build_union_policy", "evict_union_curve",
-                      "evict_profile_cost", "evict_verify_sample"):
+                      "evict_profile_cost", "evict_verify_sample", "evict_dispatch_create",
+                      "evict_dispatch_launch"):
                 getattr(L, f).restype = ctypes.c_int
             _lib = L
     return _lib
@@ -389,6 +394,42 @@ def evict_verify_sample(verify_offsets, next_token, next_sibling, retrieve_index
                                    _p(out["status"]), _stream(stream))
     _check(rc, "evict_verify_sample")
     return out
+
+
+# ----------------------------------------------------------------- verify-graph dispatch (NEXT-4)
+class VerifyDispatch:
+    """One CUDA graph: [pre] → device-side choice of the verify graph → SWITCH over the bodies.
+
+    lengths: ascending verification lengths, one per body; bodies: torch.cuda.CUDAGraph objects
+    captured with keep_graph=True (their cudaGraph_t is cloned); pre: optional CUDAGraph run first;
+    rows: int32 CUDA tensor whose first element is the step's verify row count at launch
+    (e.g. verify_offsets[B:]); chosen: int32 CUDA tensor [1] receiving the body index (or -1)."""
+
+    def __init__(self, lengths, bodies, rows, chosen=None, pre=None):
+        assert len(lengths) == len(bodies) >= 1
+        n = len(lengths)
+        self._lens = (ctypes.c_int32 * n)(*[int(x) for x in lengths])
+        self._bodies = (ctypes.c_void_p * n)(*[int(b.raw_cuda_graph()) for b in bodies])
+        self._keep = (rows, chosen, bodies, pre)
+        self._h = ctypes.c_void_p()
+        rc = lib().evict_dispatch_create(n, self._lens, self._bodies,
+                                         ctypes.c_void_p(int(pre.raw_cuda_graph())) if pre is not None else None,
+                                         _p(rows), _p(chosen), ctypes.byref(self._h))
+        _check(rc, "evict_dispatch_create")
+
+    def launch(self, stream=None):
+        _check(lib().evict_dispatch_launch(self._h, _stream(stream)), "evict_dispatch_launch")
+
+    def close(self):
+        if self._h:
+            lib().evict_dispatch_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover
+            pass
 
 
 # ----------------------------------------------------------------- router (A8 → A7)

@@ -4,7 +4,7 @@
 // tokens; C(k) is profiled offline per k).
 //
 // k_union_curve: one warp per tree, lane = layer (rounds of 32 layers), the
-// layer's expert set in registers (4 words, E ≤ 128; 8 words for masks of
+// layer's expert set in registers (4 words for ids of E ≤ 128; 8 words for ids or masks of
 // E ≤ 256), nodes visited in ranking order: each node ORs its ids into its
 // layers' sets, counts the new bits, and a warp sum gives curve[k−1].  No
 // shared memory, no atomics; each lane owns its layers exclusively.
@@ -22,22 +22,33 @@ namespace curve {
 
 constexpr int kWarpsC = 8;
 
-// OR expert e into a 4-word set; returns 1 if it was new.
-__device__ __forceinline__ uint32_t set4(uint32_t (&w)[4], uint32_t e)
+// OR expert e into an NW-word set (NW = 4: E ≤ 128, NW = 8: E ≤ 256); returns 1 if it was new.
+template <int NW>
+__device__ __forceinline__ uint32_t set4(uint32_t (&w)[NW], uint32_t e)
 {
     const uint32_t bit = 1u << (e & 31u), q = e >> 5;
-    const uint32_t cur = q == 0 ? w[0] : q == 1 ? w[1] : q == 2 ? w[2] : w[3];
+    uint32_t cur = 0u;
 #pragma unroll
-    for (int i = 0; i < 4; i++) w[i] |= (q == (uint32_t)i) ? bit : 0u;
+    for (int i = 0; i < NW; i++) cur |= (q == (uint32_t)i) ? w[i] : 0u;
+#pragma unroll
+    for (int i = 0; i < NW; i++) w[i] |= (q == (uint32_t)i) ? bit : 0u;
     return (cur & bit) ? 0u : 1u;
 }
 
-template <int IDF, int R>
+// PTX shl.b32 clamps shift amounts ≥ 32 to 32 (result 0)
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t sh)
+{
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(sh));
+    return r;
+}
+
+template <int IDF, int R, int NW>
 __global__ void __launch_bounds__(kWarpsC * 32) k_union_curve(evict_trees_t tr, const int32_t *order,
                                                               evict_routing_t rt, int32_t *curve,
                                                               int32_t *curve_layer, uint32_t *status)
 {
-    constexpr int NW = IDF == EVICT_ID_MASK ? 8 : 4;    // 32-bit words per layer set
+    static_assert(IDF != EVICT_ID_MASK || NW == 8, "mask sets span 256 experts");
     const int lane = threadIdx.x & 31;
     const int b = blockIdx.x * kWarpsC + (threadIdx.x >> 5);
     if (b >= tr.batch) return;
@@ -56,6 +67,78 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_union_curve(evict_trees_t tr, 
     }
     int tot = 0, kdone = 0;
     const int EW = (E + 63) >> 6;
+    if constexpr (IDF == EVICT_ID_U8) {
+        if (!st && K == 8) {
+            // u8 top-8 fast path: the order row lives in registers, and the routing rows of D
+            // nodes are loaded before any is processed (D independent 8-byte loads per lane
+            // and layer round in flight instead of one dependent chain per node)
+            constexpr int D = 8;
+            const int32_t *orow = order + (size_t)b * N;
+            int oreg[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) oreg[i] = lane + 32 * i < n ? __ldg(orow + lane + 32 * i) : 0;
+            const uint8_t *base = reinterpret_cast<const uint8_t *>(rt.ids) + (size_t)b * N * L * 8;
+            for (int j0 = 0; j0 < n; j0 += D) {
+                uint2 x[D][R];
+                bool badk = false;
+#pragma unroll
+                for (int h = 0; h < D; h++) {
+                    const int j = j0 + h;
+                    const int sel = (j >> 5) & 3;
+                    const int o = sel == 0 ? oreg[0] : sel == 1 ? oreg[1] : sel == 2 ? oreg[2] : oreg[3];
+                    const int v = __shfl_sync(0xffffffffu, o, j & 31);
+                    bool ok = j < n;
+                    if (ok && (v < 0 || v >= n)) { badk = true; ok = false; }
+#pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        const int l = lane + 32 * c;
+                        x[h][c] = (ok && l < L) ? __ldg(reinterpret_cast<const uint2 *>(base + ((size_t)v * L + l) * 8))
+                                                : make_uint2(0u, 0u);
+                    }
+                }
+                if (badk) { st |= EVICT_TREE_BAD_KEEP; break; }    // v is warp-uniform
+                uint32_t bad = 0;
+#pragma unroll
+                for (int h = 0; h < D; h++) {
+                    const int j = j0 + h;
+                    if (j >= n) break;
+                    uint32_t nw = 0;
+#pragma unroll
+                    for (int c = 0; c < R; c++) {
+                        const int l = lane + 32 * c;
+                        if (l >= L) continue;
+                        // one-hot words by clamped shifts: shl.b32 by ≥ 32 (incl. a negative
+                        // offset seen unsigned) is 0, so word i takes bit e − 32i only when
+                        // 32i ≤ e < 32i + 32 — no selects, no per-id "was it new" test
+                        uint32_t m[NW];
+#pragma unroll
+                        for (int i = 0; i < NW; i++) m[i] = 0u;
+#pragma unroll
+                        for (int q = 0; q < 8; q++) {
+                            const uint32_t e = __byte_perm(q < 4 ? x[h][c].x : x[h][c].y, 0, 0x4440 | (q & 3));
+                            bad |= e >= (uint32_t)E;
+#pragma unroll
+                            for (int i = 0; i < NW; i++) m[i] |= shl_clamp(1u, e - 32u * i);
+                        }
+                        int cnt = 0;
+#pragma unroll
+                        for (int i = 0; i < NW; i++) {
+                            w[c][i] |= m[i];
+                            cnt += __popc(w[c][i]);
+                        }
+                        nw += (uint32_t)(cnt - per[c]);
+                        per[c] = cnt;
+                        if (lrow) lrow[(size_t)j * L + l] = per[c];
+                    }
+                    tot += (int)__reduce_add_sync(0xffffffffu, nw);
+                    if (lane == 0) crow[j] = tot;
+                }
+                if (__any_sync(0xffffffffu, bad)) { st |= EVICT_TREE_BAD_EXPERT; break; }
+                kdone = min(n, j0 + D);
+            }
+            goto finish;
+        }
+    }
     if (!st) {
         for (int j = 0; j < n; j++) {
             const int v = __ldg(order + (size_t)b * N + j);
@@ -119,6 +202,7 @@ __global__ void __launch_bounds__(kWarpsC * 32) k_union_curve(evict_trees_t tr, 
             kdone = j + 1;
         }
     }
+finish:
     // pads (and, on error, every row) are 0
     const int from = st ? 0 : kdone;
     for (int j = from + lane; j < N; j += 32) crow[j] = 0;
@@ -186,7 +270,7 @@ extern "C" evict_status_t evict_union_curve(const evict_trees_t *trees, const in
         if (rt->num_experts > EVICT_MAX_EXPERTS) return EVICT_ERR_INVALID_ARG;
     } else if (rt->id_format == EVICT_ID_U8 || rt->id_format == EVICT_ID_I32) {
         if (rt->top_k < 1 || rt->top_k > EVICT_MAX_TOPK || rt->top_k > rt->num_experts) return EVICT_ERR_INVALID_ARG;
-        if (rt->num_experts > 128) return EVICT_ERR_UNSUPPORTED;   // 4-word register sets
+        if (rt->num_experts > EVICT_MAX_EXPERTS) return EVICT_ERR_INVALID_ARG;
     } else {
         return EVICT_ERR_INVALID_ARG;
     }
@@ -195,16 +279,17 @@ extern "C" evict_status_t evict_union_curve(const evict_trees_t *trees, const in
     cudaStream_t s = (cudaStream_t)stream;
     const int blocks = (trees->batch + kWarpsC - 1) / kWarpsC;
     const int R = (rt->num_layers + 31) / 32;
-#define EVICT_CURVE(IDFV)                                                                               \
+#define EVICT_CURVE(IDFV, NWV)                                                                         \
     switch (R) {                                                                                      \
-    case 1: k_union_curve<IDFV, 1><<<blocks, kWarpsC * 32, 0, s>>>(*trees, order, *rt, curve, curve_layer, status); break; \
-    case 2: k_union_curve<IDFV, 2><<<blocks, kWarpsC * 32, 0, s>>>(*trees, order, *rt, curve, curve_layer, status); break; \
-    case 3: k_union_curve<IDFV, 3><<<blocks, kWarpsC * 32, 0, s>>>(*trees, order, *rt, curve, curve_layer, status); break; \
-    default: k_union_curve<IDFV, 4><<<blocks, kWarpsC * 32, 0, s>>>(*trees, order, *rt, curve, curve_layer, status); break; \
+    case 1: k_union_curve<IDFV, 1, NWV><<<blocks, kWarpsC * 32, 0, s>>>(*trees, order, *rt, curve, curve_layer, status); break; \
+    case 2: k_union_curve<IDFV, 2, NWV><<<blocks, kWarpsC * 32, 0, s>>>(*trees, order, *rt, curve, curve_layer, status); break; \
+    case 3: k_union_curve<IDFV, 3, NWV><<<blocks, kWarpsC * 32, 0, s>>>(*trees, order, *rt, curve, curve_layer, status); break; \
+    default: k_union_curve<IDFV, 4, NWV><<<blocks, kWarpsC * 32, 0, s>>>(*trees, order, *rt, curve, curve_layer, status); break; \
     }
-    if (rt->id_format == EVICT_ID_U8) { EVICT_CURVE(EVICT_ID_U8) }
-    else if (rt->id_format == EVICT_ID_I32) { EVICT_CURVE(EVICT_ID_I32) }
-    else { EVICT_CURVE(EVICT_ID_MASK) }
+    const bool wide = rt->num_experts > 128;   // 8-word register sets (Ling-flash-2.0: 256 experts)
+    if (rt->id_format == EVICT_ID_U8) { if (wide) { EVICT_CURVE(EVICT_ID_U8, 8) } else { EVICT_CURVE(EVICT_ID_U8, 4) } }
+    else if (rt->id_format == EVICT_ID_I32) { if (wide) { EVICT_CURVE(EVICT_ID_I32, 8) } else { EVICT_CURVE(EVICT_ID_I32, 4) } }
+    else { EVICT_CURVE(EVICT_ID_MASK, 8) }
 #undef EVICT_CURVE
     return cudaGetLastError() == cudaSuccess ? EVICT_OK : EVICT_ERR_CUDA;
 }

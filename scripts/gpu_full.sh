@@ -1,0 +1,6 @@
+# all GPU tests + the default bench line (+ extras) + smoke
+set -x
+nvidia-smi --query-gpu=clocks.sm,clocks.max.sm --format=csv
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -8
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json

@@ -22,21 +22,22 @@ def T(a):
 
 
 @pytest.mark.parametrize("fmt", ["u8", "i32", "mask"])
-@pytest.mark.parametrize("name", ["c2", "c4", "toy_like"])
+@pytest.mark.parametrize("name", ["c2", "c4", "toy_like", "ling"])
 def test_union_curve_matches_oracle(ev, fmt, name):
     if name == "toy_like":
         B, N, steps, topk, L, E, K = 50, 8, 3, 2, 2, 8, 2
+    elif name == "ling":                  # Ling-flash-2.0: 256 experts, top-8
+        B, N, steps, topk, L, E, K = 120, 60, 6, 10, 32, 256, 8
     else:
         c = gen.CONFIGS[name]
         B, N, steps, topk, L, E, K = 120, c["N"], c["steps"], c["topk"], c["L"], c["E"], c["K"]
     P, Q, n = gen.trees(41, B, N, steps, topk)
     n[::9] = np.maximum(1, n[::9] // 3)
     ids = gen.routing(42, B, N, L, E, K, dtype=np.int32 if fmt == "i32" else np.uint8)
-    sel = ev.evict_select(T(P), T(Q), T(gen.cost_table(N)), n_nodes=T(n), with_order=True)
-    order = sel["order"]
+    order = oracle.select(P, Q, gen.cost_table(N), n_nodes=n, threads=8)["order"]   # the oracle's ranking
     dev_ids = T(gen.ids_to_mask(ids, E).view(np.int64)) if fmt == "mask" else T(ids)
-    g = ev.evict_union_curve(order, dev_ids, E, n_nodes=T(n), per_layer=True)
-    o = oracle.union_curve(order.cpu().numpy(), ids.astype(np.uint8) if fmt != "i32" else ids, E,
+    g = ev.evict_union_curve(T(order), dev_ids, E, n_nodes=T(n), per_layer=True)
+    o = oracle.union_curve(order, ids.astype(np.uint8) if fmt != "i32" else ids, E,
                            n_nodes=n, threads=8)
     assert (g["status"].cpu().numpy() == o["status"].astype(np.int32)).all()
     assert (g["curve"].cpu().numpy() == o["curve"]).all()
@@ -48,12 +49,12 @@ def test_union_curve_errors(ev):
     B, N, L, E, K = 4, 8, 2, 8, 2
     P, Q, n = gen.trees(5, B, N, 3, 2)
     ids = gen.routing(6, B, N, L, E, K)
-    order = ev.evict_select(T(P), T(Q), T(gen.cost_table(N)), n_nodes=T(n), with_order=True)["order"]
+    order = oracle.select(P, Q, gen.cost_table(N), n_nodes=n)["order"].copy()
     order[1, 0] = 99                      # not a node of tree 1
     bad = ids.copy()
     bad[2, :, 0, 0] = 200                 # id ≥ E in every node of tree 2
-    g = ev.evict_union_curve(order, T(bad), E, n_nodes=T(n), per_layer=True)
-    o = oracle.union_curve(order.cpu().numpy(), bad, E, n_nodes=n)
+    g = ev.evict_union_curve(T(order), T(bad), E, n_nodes=T(n), per_layer=True)
+    o = oracle.union_curve(order, bad, E, n_nodes=n)
     assert (g["status"].cpu().numpy() == o["status"].astype(np.int32)).all()
     assert o["status"][1] and o["status"][2]
     assert (g["curve"].cpu().numpy() == o["curve"]).all()
@@ -70,11 +71,13 @@ def test_profile_cost_matches_oracle_and_feeds_select(ev):
     sel = ev.evict_select(T(P), T(Q), T(gen.cost_table(N)), n_nodes=T(n), with_order=True)
     g = ev.evict_union_curve(sel["order"], T(ids), E, n_nodes=T(n))
     cost = ev.evict_profile_cost(g["curve"], L, n_nodes=T(n), status=g["status"]).cpu().numpy()
-    oc = oracle.profile_cost(g["curve"].cpu().numpy(), L, n_nodes=n, status=g["status"].cpu().numpy())
+    osel = oracle.select(P, Q, gen.cost_table(N), n_nodes=n, threads=8)           # oracle chain end to end
+    ocur = oracle.union_curve(osel["order"], ids, E, n_nodes=n, threads=8, per_layer=False)
+    oc = oracle.profile_cost(ocur["curve"], L, n_nodes=n, status=ocur["status"])
     fin = np.isfinite(oc)
     assert (np.isfinite(cost) == fin).all()
     assert np.allclose(cost[fin], oc[fin].astype(np.float32), rtol=2 ** -23, atol=0)
     s2 = ev.evict_select(T(P), T(Q), T(cost), n_nodes=T(n), with_order=True)
-    o2 = oracle.select(P, Q, cost, n_nodes=n, threads=8)
+    o2 = oracle.select(P, Q, oc.astype(np.float32), n_nodes=n, threads=8)
     res, msgs = compare_select(o2, {k: v.cpu().numpy() for k, v in s2.items()}, n_nodes=n, check_order=True)
     assert not msgs, msgs[:3]

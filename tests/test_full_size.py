@@ -6,7 +6,7 @@ import pytest
 
 import gen
 import oracle
-from oracle.parity import compare_build, compare_select, compare_union
+from oracle.parity import downstream_keep, compare_build, compare_select, compare_union
 
 pytestmark = pytest.mark.gpu
 
@@ -56,7 +56,7 @@ def test_sampled_blocks_match_oracle(sweep, block):
     o = oracle.select(P, Q, gen.cost_table(N), n_nodes=n, threads=8)
     res, msgs = compare_select(o, g, n_nodes=n)
     assert not msgs, msgs[:3]
-    keep = g["keep_bits"].view(np.uint64)
+    keep = downstream_keep(o, g)
     assert not compare_union(oracle.expert_union(keep, ids, E, n_nodes=n, threads=8), g)
     # packed verify rows of the block, relative to the block's first offset
     off = out["verify_offsets"][lo:lo + B + 1].cpu().numpy().astype(np.int64)

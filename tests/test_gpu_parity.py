@@ -12,7 +12,7 @@ import pytest
 
 import gen
 import oracle
-from oracle.parity import compare_build, compare_select, compare_union
+from oracle.parity import downstream_keep, compare_build, compare_select, compare_union
 
 pytestmark = pytest.mark.gpu
 
@@ -289,7 +289,7 @@ def test_fused_equals_oracle(ev, name, fmt, with_order):
     o = oracle.select(P, Q, cost, n_nodes=n, threads=8)
     res, msgs = compare_select(o, g, n_nodes=n, check_order=with_order)
     assert not msgs, msgs[:5]
-    keep = g["keep_bits"].view(np.uint64)
+    keep = downstream_keep(o, g)
     ob = oracle.build_verify_tree(P, keep, n_nodes=n, pos_offset=pos)
     assert not compare_build(ob, {k: v for k, v in g.items() if k != "status"})
     ou = oracle.expert_union(keep, ids, E, n_nodes=n, threads=8)
@@ -399,7 +399,7 @@ def test_fused_policy_vs_oracle(ev, policy, with_order):
     o = oracle.select(P, Q, cost, n_nodes=n, threads=8, policy=policy)
     res, msgs = compare_select(o, g, n_nodes=n, check_order=with_order)
     assert not msgs, msgs[:5]
-    keep = g["keep_bits"].view(np.uint64)
+    keep = downstream_keep(o, g)
     assert not compare_build(oracle.build_verify_tree(P, keep, n_nodes=n),
                              {k: v for k, v in g.items() if k != "status"})
     assert not compare_union(oracle.expert_union(keep, ids, E, n_nodes=n, threads=8), g)
