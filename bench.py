@@ -324,6 +324,28 @@ def time_fused(ev, torch, call, stream, reps):
     return e0.elapsed_time(e1) / reps
 
 
+def ling_variant(ev, gen, torch, P, Q, n, cost, M, stream, reps):
+    """NEXT-4 model shape: the same trees with Ling-flash-2.0-shaped routing (256 experts top-8,
+    PAPER.md:557; 32 MoE layers), u8 ids [M][60][32][8] (15.4 KB per tree), fused
+    select → build → union with 4-word expert sets."""
+    L, E = 32, 256
+    ids = gen.routing_cuda(6, M, P.shape[1], L, E, TOP_K)
+    call = ev.FusedCall(P, Q, cost, ids, E, n_nodes=n)
+    ms = time_fused(ev, torch, call, stream, reps)
+    k_sum = int(call.buffers.t["k_star"].sum())
+    n_sum = int(n.sum())
+    abytes, parts = algorithmic_bytes(n_sum, k_sum, M, 1, L=L, EW=4)
+    peak, _ = hbm_peak()
+    ach = abytes / (ms / 1e3) / 1e9
+    um = float(call.buffers.t["union_total"].double().mean()) / L
+    del call, ids
+    torch.cuda.empty_cache()
+    return {"model": "Ling-flash-2.0-shaped (L 32, E 256, top-8)", "id_format": "u8", "value": M / (ms / 1e3),
+            "unit": "trees/s", "kernel_ms": ms, "k_sum": k_sum, "union_mean_per_layer": um,
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "algorithmic_bytes_per_launch": abytes}}
+
+
 def mask_variant(ev, gen, torch, P, Q, n, cost, ids8, M, stream, reps):
     """Same trees with routing re-encoded as one-hot expert masks (16 B per node-layer):
     the union becomes a pure OR stream."""
@@ -539,15 +561,17 @@ def router_bench(ev, gen, torch, stream):
     peaks_ = peaks()
     tf_peak = float(peaks_.get("bf16_tflops", 1590.0))
     hbm, _ = hbm_peak()
-    for name, B, Nn, steps, topk, L, d in (("c2", 1, 60, 6, 10, 48, 2048),
-                                            ("c3_b16", 16, 60, 6, 10, 94, 4096),
-                                            ("c4", 64, 128, 8, 10, 48, 2048)):
+    for name, B, Nn, steps, topk, L, d, E in (("c2", 1, 60, 6, 10, 48, 2048, 128),
+                                               ("c3_b16", 16, 60, 6, 10, 94, 4096, 128),
+                                               ("c4", 64, 128, 8, 10, 48, 2048, 128),
+                                               ("ling_b1", 1, 60, 6, 10, 32, 4096, 256),
+                                               ("ling_b16", 16, 60, 6, 10, 32, 4096, 256)):
         P, Q, n = gen.trees(3, B, Nn, steps, topk)
         cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
         sel = ev.evict_select(cu(P), cu(Q), cu(gen.cost_table(Nn)), n_nodes=cu(n))
         b = ev.evict_build_verify_tree(cu(P), sel["keep_bits"], n_nodes=cu(n))
         h = gen.hidden_cuda(11, B, Nn, L, d, mode=1)
-        w = gen.wgate_cuda(12, L, N_EXPERTS, d, mode=1, scale_log2=-5)
+        w = gen.wgate_cuda(12, L, E, d, mode=1, scale_log2=-5)
         T = int(b["verify_offsets"][-1])
         rc = ev.RouterCall(b["verify_offsets"], b["retrieve_index"], h, w, TOP_K, B, Nn, max_rows=T)
         for _ in range(3):
@@ -561,12 +585,12 @@ def router_bench(ev, gen, torch, stream):
         e1.record(stream)
         e1.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / reps
-        byt = L * (T * d + N_EXPERTS * d) * 2
-        fl = 2.0 * L * T * d * N_EXPERTS
-        res[name] = {"B": B, "N": Nn, "L": L, "d": d, "rows": T, "us": us,
+        byt = L * (T * d + E * d) * 2
+        fl = 2.0 * L * T * d * E
+        res[name] = {"B": B, "N": Nn, "L": L, "d": d, "E": E, "rows": T, "us": us,
                      "gbs": byt / (us / 1e6) / 1e9, "hbm_frac": byt / (us / 1e6) / 1e9 / hbm,
                      "tflops": fl / (us / 1e6) / 1e12, "tensor_frac": fl / (us / 1e6) / 1e12 / tf_peak,
-                     "bound": "hbm (intensity <= E = 128 flop/B < ridge)"}
+                     "bound": f"hbm (intensity <= E = {E} flop/B; ridge 220)"}
         del h, w
     torch.cuda.empty_cache()
     return res
@@ -696,6 +720,10 @@ def run_native(args, rank, world, local_rank):
                                                        max(3, K // 2))}
         except Exception as e:  # pragma: no cover
             result["variants"] = {"mask": {"error": repr(e)}}
+        try:
+            result["variants"]["ling"] = ling_variant(ev, gen, torch, P, Q, n, cost, M, stream, max(3, K // 2))
+        except Exception as e:  # pragma: no cover
+            result["variants"]["ling"] = {"error": repr(e)}
         try:
             result["policies"] = policy_variants(ev, torch, P, Q, n, cost, ids, M, stream, max(3, K // 2))
         except Exception as e:  # pragma: no cover

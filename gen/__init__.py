@@ -37,6 +37,8 @@ CONFIGS = {
     "c4_60": dict(B=64, N=60, steps=6, topk=10, L=48, E=128, K=8, d=2048, seed=4),
     "c5": dict(B=1_000_000, N=60, steps=6, topk=10, L=48, E=128, K=8, d=2048, seed=5),
     "paper": dict(B=1, N=32, steps=4, topk=8, L=48, E=128, K=8, d=2048, seed=7),
+    # Ling-flash-2.0 (256 experts, top-8; 32 MoE layers, hidden 4096) — NEXT-4 shape
+    "ling": dict(B=1, N=60, steps=6, topk=10, L=32, E=256, K=8, d=4096, seed=6),
 }
 M_LO, M_HI = 1, 16          # per-tree difficulty exponent range (evict_gen.h)
 SIGMA_Q4 = 9                # round(4 * sigma_b), sigma_b = 2.25

@@ -256,7 +256,8 @@ evict_status_t evict_select_build_union_policy(const evict_trees_t *trees, const
  *            launch only (grid, k-split, ring depth).  Contract: T ≤
  *            max_rows (T is device-resident, so the host cannot check it;
  *            rows at or past ceil(max_rows/128)·128 would not be routed).
- * Supported: E = 128, d % 64 == 0, K ≤ 16, L·B·N < 2^31.
+ * Supported: E ∈ {128, 256} (256: Ling-flash-2.0; N = 256 MMA,
+ *   union_bits [B][L][4]), d % 64 == 0, K ≤ 16, L·B·N < 2^31.
  * ------------------------------------------------------------------------- */
 typedef struct {
     int32_t num_layers;

@@ -26,18 +26,19 @@
 namespace evict {
 namespace router {
 
-constexpr int BM = 128, BN = 128, BK = 64;
+constexpr int BM = 128, BK = 64;   // rows per tile, k-block; the MMA N = E (128 or 256, template NE)
 // operand ring depth (template): 6 stages (1 CTA/SM) when the grid fits one wave,
 // 3 stages (2 CTAs/SM, 256 of 512 TMEM columns) when tiles × layers exceed the SMs
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_BYTES = BN * BK * 2;  // 16 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+template <int NE> __host__ __device__ constexpr int b_bytes() { return NE * BK * 2; }            // 16 / 32 KB
+template <int NE> __host__ __device__ constexpr int stage_bytes() { return A_BYTES + b_bytes<NE>(); }
 constexpr int THREADS = 192;
 constexpr int NPROD = 128;
 constexpr int KMAX = 16;
+template <int NE>
 __host__ __device__ constexpr int smem_bytes(int stages)
 {
-    return stages * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers, ridx*/ + 512;
+    return stages * stage_bytes<NE>() + 1024 /*align*/ + 1024 /*barriers, ridx*/ + 512;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -128,11 +129,14 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t addr)
     return (uint64_t)((addr & 0x3FFFFu) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
 }
 
-// Instruction descriptor: kind::f16, A/B bf16, D fp32, K-major, M=128, N=128.
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// Instruction descriptor: kind::f16, A/B bf16, D fp32, K-major, M=128, N=NE.
+template <int NE>
+__host__ __device__ constexpr uint32_t idesc() { return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NE >> 3) << 17) | ((uint32_t)(BM >> 4) << 24); }
 
+template <int NE>
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate)
 {
+    constexpr uint32_t kIdesc = idesc<NE>();
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
@@ -171,9 +175,16 @@ __device__ __forceinline__ long long gtimer()
     return t;
 }
 
-template <int KL>
-__device__ __forceinline__ uint4 topk_scan(const float *lg, int K, bool valid, int32_t *out, long long *tr)
+// Expert bitset of one row: NE/32 words (scalars in registers after unrolling).
+template <int NE>
+struct Bits {
+    uint32_t w[NE / 32];
+};
+
+template <int KL, int NE>
+__device__ __forceinline__ Bits<NE> topk_scan(const float *lg, int K, bool valid, int32_t *out, long long *tr)
 {
+    constexpr int BN = NE;
     // Candidates are visited in expert order, so a new candidate loses every tie:
     // its rank is p = #{j < K : bv[j] >= v}; p == K never happens for a candidate
     // (it beats the K-th entry or the list is not full).  Insertion is a branch-free shift by
@@ -244,22 +255,22 @@ __device__ __forceinline__ uint4 topk_scan(const float *lg, int K, bool valid, i
         }
     }
     if (tr) { tr[199] = gtimer(); tr[200] = nins; tr[201] = clock64() - c0; }
-    // scalar words (no array: the compiler would turn the word select into a
-    // dynamically indexed local-memory array)
-    uint32_t w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
+    // word select by compile-time-unrolled compares (a dynamically indexed word
+    // would turn the set into a local-memory array)
+    Bits<NE> r;
+#pragma unroll
+    for (int q = 0; q < NE / 32; q++) r.w[q] = 0u;
 #pragma unroll
     for (int j = 0; j < KL; j++) {
         const int e = bi[j];
         const bool ok = j < K && e >= 0 && e < BN;
         const uint32_t bit = ok ? (1u << (e & 31)) : 0u;
         const int q = e >> 5;
-        w0 |= q == 0 ? bit : 0u;
-        w1 |= q == 1 ? bit : 0u;
-        w2 |= q == 2 ? bit : 0u;
-        w3 |= q == 3 ? bit : 0u;
+#pragma unroll
+        for (int qq = 0; qq < NE / 32; qq++) r.w[qq] |= q == qq ? bit : 0u;
         if (ok && valid && out) out[j] = e;
     }
-    return make_uint4(w0, w1, w2, w3);
+    return r;
 }
 
 // TopK of one row by a whole warp (sparse tiles: few valid rows would leave one
@@ -272,35 +283,39 @@ __device__ __forceinline__ uint32_t f2ord(float f)
     const uint32_t b = __float_as_uint(f);
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
-__device__ __forceinline__ uint4 topk_warp_row(const float *lgrow, int K, int32_t *out, int lane)
+template <int NE>
+__device__ __forceinline__ Bits<NE> topk_warp_row(const float *lgrow, int K, int32_t *out, int lane)
 {
-    float v[4];
+    constexpr int Q = NE / 32;
+    float v[Q];
 #pragma unroll
-    for (int q = 0; q < 4; q++) v[q] = lgrow[lane + 32 * q];
-    uint32_t w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
+    for (int q = 0; q < Q; q++) v[q] = lgrow[lane + 32 * q];
+    Bits<NE> r;
+#pragma unroll
+    for (int q = 0; q < Q; q++) r.w[q] = 0u;
     const float ninf = -__int_as_float(0x7f800000);
 #pragma unroll 1
     for (int j = 0; j < K; j++) {
-        const float m = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+        float m = v[0];
+#pragma unroll
+        for (int q = 1; q < Q; q++) m = fmaxf(m, v[q]);
         const uint32_t u = f2ord(m);
         const uint32_t U = __reduce_max_sync(0xffffffffu, u);
-        int el = 255;
+        int el = 0xffff;
 #pragma unroll
-        for (int q = 3; q >= 0; q--) el = (v[q] == m) ? lane + 32 * q : el;
-        const int e = (int)__reduce_min_sync(0xffffffffu, u == U ? (uint32_t)el : 255u);
+        for (int q = Q - 1; q >= 0; q--) el = (v[q] == m) ? lane + 32 * q : el;
+        const int e = (int)__reduce_min_sync(0xffffffffu, u == U ? (uint32_t)el : 0xffffu);
         if ((e & 31) == lane) {
 #pragma unroll
-            for (int q = 0; q < 4; q++) v[q] = (q == (e >> 5)) ? ninf : v[q];
+            for (int q = 0; q < Q; q++) v[q] = (q == (e >> 5)) ? ninf : v[q];
         }
         const uint32_t bit = 1u << (e & 31);
         const int qw = e >> 5;
-        w0 |= qw == 0 ? bit : 0u;
-        w1 |= qw == 1 ? bit : 0u;
-        w2 |= qw == 2 ? bit : 0u;
-        w3 |= qw == 3 ? bit : 0u;
+#pragma unroll
+        for (int q = 0; q < Q; q++) r.w[q] |= qw == q ? bit : 0u;
         if (out && lane == 0) out[j] = e;
     }
-    return make_uint4(w0, w1, w2, w3);
+    return r;
 }
 
 struct Params {
@@ -309,17 +324,20 @@ struct Params {
     const int32_t *retrieve_index; // [cap]
     int L, B, N, d, K;
     int splits;                    // k-splits = cluster size along z (1: no cluster)
-    unsigned long long *bits;      // [B][L][2]
+    unsigned long long *bits;      // [B][L][NE/64]
     int32_t *topk_ids;             // [L][B*N][K] or null
     float *dbg_logits;             // [L][B*N][128] or null (debug entry point only)
     long long *trace;              // [256] globaltimer trace of CTA (0,0) or null (debug only)
 };
 
 
-template <int STAGES>
+template <int NE, int STAGES>
 __global__ void __launch_bounds__(THREADS, STAGES <= 3 ? 2 : 1)
 k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap hmap, Params p)
 {
+    constexpr int BN = NE, EW = NE / 64;
+    constexpr int B_BYTES = b_bytes<NE>(), STAGE_BYTES = stage_bytes<NE>();
+    static_assert(BM * (BN + 1) * 4 <= STAGES * STAGE_BYTES, "logit staging must fit the operand ring");
     extern __shared__ uint8_t smem_raw[];
     const int T = __ldg(p.verify_offsets + p.B);
     const int m0 = blockIdx.x * BM;
@@ -351,7 +369,7 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 4) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)) : "memory");
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(NE) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (threadIdx.x < BM) {
@@ -418,7 +436,7 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                 for (int k = 0; k < BK / 16; k++)
-                    umma_bf16(tmem, umma_desc(A(s) + 32 * k), umma_desc(Bs(s) + 32 * k), (i | k) != 0);
+                    umma_bf16<NE>(tmem, umma_desc(A(s) + 32 * k), umma_desc(Bs(s) + 32 * k), (i | k) != 0);
                 umma_commit(empty0 + 8 * s);
             }
             umma_commit(tfull);
@@ -456,7 +474,7 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
     if (tr0 && threadIdx.x == 0) p.trace[195] = gtimer();
     if (warp == 4) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(NE) : "memory");
     }
     if (S > 1) cluster_sync();                // every split's partial is staged
 
@@ -493,19 +511,20 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
                 const int rg = m0 + rr;
                 int32_t *o = p.topk_ids ? p.topk_ids + ((size_t)l * BNrows + rg) * p.K : nullptr;
                 const float *lrow = reinterpret_cast<const float *>(base) + (size_t)rr * (BN + 1);
-                const uint4 wr = topk_warp_row(lrow, p.K, o, lane);
+                const Bits<NE> wr = topk_warp_row<NE>(lrow, p.K, o, lane);
                 if (lane == 0) {
-                    unsigned long long *dst = p.bits + ((size_t)(ridx[rr] / p.N) * p.L + l) * 2;
-                    atomicOr(dst, (unsigned long long)wr.x | ((unsigned long long)wr.y << 32));
-                    atomicOr(dst + 1, (unsigned long long)wr.z | ((unsigned long long)wr.w << 32));
+                    unsigned long long *dst = p.bits + ((size_t)(ridx[rr] / p.N) * p.L + l) * EW;
+#pragma unroll
+                    for (int h = 0; h < EW; h++)
+                        atomicOr(dst + h, (unsigned long long)wr.w[2 * h] | ((unsigned long long)wr.w[2 * h + 1] << 32));
                 }
             }
             if (tr0 && threadIdx.x == 0) p.trace[197] = gtimer();
         } else {
         long long *ttr = (tr0 && threadIdx.x == 0) ? p.trace : nullptr;
         int32_t *tk_out = p.topk_ids ? p.topk_ids + ((size_t)l * BNrows + r) * p.K : nullptr;
-        const uint4 wq = p.K <= 8 ? topk_scan<8>(lg, p.K, valid, tk_out, ttr) : topk_scan<KMAX>(lg, p.K, valid, tk_out, ttr);
-        const uint32_t w[4] = {wq.x, wq.y, wq.z, wq.w};
+        const Bits<NE> wq = p.K <= 8 ? topk_scan<8, NE>(lg, p.K, valid, tk_out, ttr)
+                                     : topk_scan<KMAX, NE>(lg, p.K, valid, tk_out, ttr);
         if (tr0 && threadIdx.x == 0) p.trace[197] = gtimer();
         const int tree = valid ? ridx[row] / p.N : -1;
         unsigned pending = __ballot_sync(0xffffffffu, valid);
@@ -514,13 +533,14 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
             const int tb = __shfl_sync(0xffffffffu, tree, leader);
             const unsigned grp = __ballot_sync(0xffffffffu, valid && tree == tb);
             const bool in = (grp >> lane) & 1u;
-            uint32_t o[4];
+            uint32_t o[NE / 32];
 #pragma unroll
-            for (int q = 0; q < 4; q++) o[q] = __reduce_or_sync(0xffffffffu, in ? w[q] : 0u);
+            for (int q = 0; q < NE / 32; q++) o[q] = __reduce_or_sync(0xffffffffu, in ? wq.w[q] : 0u);
             if (lane == leader) {
-                unsigned long long *dst = p.bits + ((size_t)tb * p.L + l) * 2;
-                atomicOr(dst, (unsigned long long)o[0] | ((unsigned long long)o[1] << 32));
-                atomicOr(dst + 1, (unsigned long long)o[2] | ((unsigned long long)o[3] << 32));
+                unsigned long long *dst = p.bits + ((size_t)tb * p.L + l) * EW;
+#pragma unroll
+                for (int h = 0; h < EW; h++)
+                    atomicOr(dst + h, (unsigned long long)o[2 * h] | ((unsigned long long)o[2 * h + 1] << 32));
             }
             pending &= ~grp;
         }
@@ -529,14 +549,15 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
     if (S > 1) cluster_sync();                // partials stay alive until the leader has read them
 }
 
-__global__ void k_finalize(int B, int L, const unsigned long long *bits, int32_t *count, int32_t *total)
+__global__ void k_finalize(int B, int L, int EW, const unsigned long long *bits, int32_t *count, int32_t *total)
 {
     const int b = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (b >= B) return;
     int tot = 0;
     for (int l = lane; l < L; l += 32) {
-        const int c = __popcll(bits[((size_t)b * L + l) * 2]) + __popcll(bits[((size_t)b * L + l) * 2 + 1]);
+        int c = 0;
+        for (int h = 0; h < EW; h++) c += __popcll(bits[((size_t)b * L + l) * EW + h]);
         count[(size_t)b * L + l] = c;
         tot += c;
     }
@@ -606,7 +627,7 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     if (rt->top_k < 1 || rt->top_k > EVICT_MAX_TOPK || rt->top_k > rt->num_experts) return EVICT_ERR_INVALID_ARG;
     if (rt->hidden_dim < 64 || rt->hidden_dim % 64) return EVICT_ERR_INVALID_ARG;
     if (((uintptr_t)rt->hidden | (uintptr_t)rt->w_gate) & 15) return EVICT_ERR_INVALID_ARG;
-    if (rt->num_experts != 128) return EVICT_ERR_UNSUPPORTED;
+    if (rt->num_experts != 128 && rt->num_experts != 256) return EVICT_ERR_UNSUPPORTED;
     if (evict::dev_sms() <= 0) return EVICT_ERR_UNSUPPORTED;
     EncodeTiledFn enc = encode_fn();
     if (!enc) return EVICT_ERR_UNSUPPORTED;
@@ -615,7 +636,7 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)L * E};
     cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-    cuuint32_t box[2] = {BK, BN};
+    cuuint32_t box[2] = {BK, (cuuint32_t)E};   // one W_g k-block: all E experts (≤ 256 rows)
     cuuint32_t estr[2] = {1, 1};
     if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(rt->w_gate), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -633,10 +654,12 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     cudaStream_t s = (cudaStream_t)stream;
     static std::once_flag attr_once;
     std::call_once(attr_once, [] {
-        cudaFuncSetAttribute(k_router<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(6));
-        cudaFuncSetAttribute(k_router<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes(3));
+        cudaFuncSetAttribute(k_router<128, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>(6));
+        cudaFuncSetAttribute(k_router<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>(3));
+        cudaFuncSetAttribute(k_router<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<256>(4));
     });
-    if (cudaMemsetAsync(union_bits, 0, sizeof(uint64_t) * (size_t)B * L * 2, s) != cudaSuccess) return EVICT_ERR_CUDA;
+    const int EW = E / 64;
+    if (cudaMemsetAsync(union_bits, 0, sizeof(uint64_t) * (size_t)B * L * EW, s) != cudaSuccess) return EVICT_ERR_CUDA;
     Params p;
     p.hidden = (const uint16_t *)rt->hidden;
     p.verify_offsets = verify_offsets;
@@ -659,17 +682,18 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     if (S > KB) S = KB;
     // clusters are placed GPC by GPC: take the largest S whose tiles·L clusters are all
     // co-resident (a second wave would double the time)
-    static int max_clusters[5] = {-1, -1, -1, -1, -1};
+    static int max_clusters[2][5] = {{-1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1}};
+    const int wide = E == 256;   // 256 experts: N = 256 MMA, 48 KB stages, 4-stage ring, 1 CTA/SM
     static std::mutex mc_mu;
     while (S > 1) {
         int mc;
         {
             std::lock_guard<std::mutex> g(mc_mu);
-            if (max_clusters[S] < 0) {
+            if (max_clusters[wide][S] < 0) {
                 cudaLaunchConfig_t q = {};
                 q.gridDim = dim3((unsigned)S, 1u, 1u);
                 q.blockDim = dim3(THREADS, 1, 1);
-                q.dynamicSmemBytes = smem_bytes(6);
+                q.dynamicSmemBytes = wide ? smem_bytes<256>(4) : smem_bytes<128>(6);
                 cudaLaunchAttribute a[1];
                 a[0].id = cudaLaunchAttributeClusterDimension;
                 a[0].val.clusterDim.x = (unsigned)S;
@@ -678,9 +702,11 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
                 q.attrs = a;
                 q.numAttrs = 1;
                 int n = 0;
-                max_clusters[S] = cudaOccupancyMaxActiveClusters(&n, k_router<6>, &q) == cudaSuccess ? n : 0;
+                const cudaError_t qe = wide ? cudaOccupancyMaxActiveClusters(&n, k_router<256, 4>, &q)
+                                            : cudaOccupancyMaxActiveClusters(&n, k_router<128, 6>, &q);
+                max_clusters[wide][S] = qe == cudaSuccess ? n : 0;
             }
-            mc = max_clusters[S];
+            mc = max_clusters[wide][S];
         }
         if (mc >= tiles * L) break;
         S--;
@@ -688,13 +714,14 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     p.splits = S;
     if (S == 1) {
         dim3 grid((unsigned)tiles, (unsigned)L, 1u);
-        if ((long)tiles * L > evict::dev_sms()) k_router<3><<<grid, THREADS, smem_bytes(3), s>>>(map, hmap, p);
-        else k_router<6><<<grid, THREADS, smem_bytes(6), s>>>(map, hmap, p);
+        if (wide) k_router<256, 4><<<grid, THREADS, smem_bytes<256>(4), s>>>(map, hmap, p);
+        else if ((long)tiles * L > evict::dev_sms()) k_router<128, 3><<<grid, THREADS, smem_bytes<128>(3), s>>>(map, hmap, p);
+        else k_router<128, 6><<<grid, THREADS, smem_bytes<128>(6), s>>>(map, hmap, p);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)tiles, (unsigned)L, (unsigned)S);
         cfg.blockDim = dim3(THREADS, 1, 1);
-        cfg.dynamicSmemBytes = smem_bytes(6);
+        cfg.dynamicSmemBytes = wide ? smem_bytes<256>(4) : smem_bytes<128>(6);
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -703,10 +730,12 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
         attr[0].val.clusterDim.z = (unsigned)S;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, k_router<6>, map, hmap, p) != cudaSuccess) return EVICT_ERR_CUDA;
+        const cudaError_t le = wide ? cudaLaunchKernelEx(&cfg, k_router<256, 4>, map, hmap, p)
+                                    : cudaLaunchKernelEx(&cfg, k_router<128, 6>, map, hmap, p);
+        if (le != cudaSuccess) return EVICT_ERR_CUDA;
     }
     if (cudaGetLastError() != cudaSuccess) return EVICT_ERR_CUDA;
-    k_finalize<<<(B + 7) / 8, 256, 0, s>>>(B, L, reinterpret_cast<const unsigned long long *>(union_bits),
+    k_finalize<<<(B + 7) / 8, 256, 0, s>>>(B, L, EW, reinterpret_cast<const unsigned long long *>(union_bits),
                                            union_count, union_total);
     return cudaGetLastError() == cudaSuccess ? EVICT_OK : EVICT_ERR_CUDA;
 }

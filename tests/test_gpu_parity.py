@@ -273,7 +273,7 @@ def test_union_bad_expert_and_hist(ev):
 # ------------------------------------------------------------------ fused
 @pytest.mark.parametrize("with_order", [True, False])
 @pytest.mark.parametrize("name,fmt", [("c2", "u8"), ("c4", "u8"), ("c4_60", "i32"),
-                                      ("c4_60", "mask"), ("paper", "u8")])
+                                      ("c4_60", "mask"), ("paper", "u8"), ("ling", "u8"), ("ling", "mask")])
 def test_fused_equals_oracle(ev, name, fmt, with_order):
     c = gen.CONFIGS[name]
     B = 333

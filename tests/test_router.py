@@ -27,32 +27,33 @@ def bf16(a_bits):
 
 
 def kept_rows(ev, B, N, steps, topk, seed):
+    """The oracle's Eq. 10 keep sets, compacted into packed verify rows on the GPU."""
     P, Q, n = gen.trees(seed, B, N, steps, topk)
-    cost = gen.cost_table(N)
-    sel = ev.evict_select(cu(P), cu(Q), cu(cost), n_nodes=cu(n))
-    b = ev.evict_build_verify_tree(cu(P), sel["keep_bits"], n_nodes=cu(n))
-    return P, n, sel, b
+    keep = oracle.select(P, Q, gen.cost_table(N), n_nodes=n)["keep_bits"]
+    b = ev.evict_build_verify_tree(cu(P), cu(keep.view(np.int64)), n_nodes=cu(n))
+    return P, n, keep, b
 
 
-@pytest.mark.parametrize("B,N,steps,topk,L,d,K", [
-    (1, 60, 6, 10, 48, 2048, 8),      # c2 shape
-    (16, 60, 6, 10, 6, 4096, 8),      # c3 shape, fewer layers
-    (64, 128, 8, 10, 4, 2048, 8),     # c4 shape, fewer layers
-    (5, 32, 4, 8, 3, 64, 2),          # small d, K=2
-    (3, 8, 3, 2, 2, 128, 16),         # K = 16
+@pytest.mark.parametrize("B,N,steps,topk,L,d,K,E", [
+    (1, 60, 6, 10, 48, 2048, 8, 128),     # c2 shape
+    (16, 60, 6, 10, 6, 4096, 8, 128),     # c3 shape, fewer layers
+    (64, 128, 8, 10, 4, 2048, 8, 128),    # c4 shape, fewer layers
+    (5, 32, 4, 8, 3, 64, 2, 128),         # small d, K=2
+    (3, 8, 3, 2, 2, 128, 16, 128),        # K = 16
+    (1, 60, 6, 10, 32, 4096, 8, 256),     # Ling-flash-2.0 shape (NEXT-4): 256 experts, batch 1
+    (16, 60, 6, 10, 4, 4096, 8, 256),     # 256 experts, 16 trees
+    (64, 128, 8, 10, 3, 2048, 16, 256),   # 256 experts, dense tiles, K = 16
 ])
 @pytest.mark.parametrize("hint", [False, True])
-def test_router_integer_inputs_bit_exact(ev, B, N, steps, topk, L, d, K, hint):
+def test_router_integer_inputs_bit_exact(ev, B, N, steps, topk, L, d, K, E, hint):
     """Integer-valued bf16 h, W_g ⇒ every fp32 partial sum is exact ⇒ TopK (with the
     (logit desc, expert asc) tie rule) must match the fp64 oracle bit for bit."""
-    E = 128
-    P, n, sel, b = kept_rows(ev, B, N, steps, topk, seed=21)
+    P, n, keep, b = kept_rows(ev, B, N, steps, topk, seed=21)
     h = gen.hidden(31, B, N, L, d, mode=0)
     w = gen.wgate(32, L, E, d, mode=0)
     T = int(b["verify_offsets"][-1])
     g = ev.evict_router_union(b["verify_offsets"], b["retrieve_index"], bf16(h), bf16(w), K, B, N,
                               with_topk=True, max_rows=T if hint else 0)   # the hint resizes the launch
-    keep = sel["keep_bits"].cpu().numpy().view(np.uint64)
     o = oracle.router_union(keep, h, w, K, threads=8)
     gg = {k: v.cpu().numpy() for k, v in g.items()}
     assert not compare_union(o, gg)
@@ -66,12 +67,13 @@ def test_router_integer_inputs_bit_exact(ev, B, N, steps, topk, L, d, K, hint):
             assert gg["topk_ids"][l, r].tolist() == ids.tolist(), (l, r)
 
 
-def test_router_vs_torch_normal_inputs(ev):
+@pytest.mark.parametrize("E", [128, 256])
+def test_router_vs_torch_normal_inputs(ev, E):
     """bf16 N(0,1) inputs: compare with the library routine torch.matmul (fp32) + torch.topk,
     excluding rows whose K-th/(K+1)-th logit gap is within fp32 accumulation error."""
     import torch
-    B, N, L, d, K, E = 16, 60, 5, 2048, 8, 128
-    P, n, sel, b = kept_rows(ev, B, N, 6, 10, seed=5)
+    B, N, L, d, K = 16, 60, 5, 2048, 8
+    P, n, keep, b = kept_rows(ev, B, N, 6, 10, seed=5)
     h = gen.hidden_cuda(41, B, N, L, d, mode=1)
     w = gen.wgate_cuda(42, L, E, d, mode=1, scale_log2=-5)
     g = ev.evict_router_union(b["verify_offsets"], b["retrieve_index"], h, w, K, B, N, with_topk=True)
