@@ -553,6 +553,38 @@ def dispatch_bench(ev, gen, torch):
     return res
 
 
+def draft_bench(ev, torch, stream):
+    """NEXT-4 (P2): draft-tree builder on EAGLE-3-shaped drafter tables (steps 6, topk 10,
+    budget 60 — the C2/C5 trees).  Algorithmic bytes per tree: table in steps·topk²·8 B
+    (tokens + probs, 4.8 KB) + rows out 12·N + 8 B.  65,536 trees (315 MB ≫ L2) for throughput;
+    batch-64 latency by CUDA events (inputs L2-resident after the first call)."""
+    import numpy as np
+    from gen.draft import drafter_tables
+    steps, topk, N = 6, 10, 60
+    res = {}
+    for name, B in (("b64", 64), ("b65536", 65536)):
+        tok, pr = drafter_tables(13, B, steps, topk)
+        t, p = torch.from_numpy(tok).cuda(), torch.from_numpy(pr).cuda()
+        out = ev.evict_build_draft_tree(t, p, N, stream=stream)
+        reps = 20
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            ev.evict_build_draft_tree(t, p, N, out=out, stream=stream)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        byt = B * (steps * topk * topk * 8 + 12 * N + 8)
+        peak, _ = hbm_peak()
+        ach = byt / (ms / 1e3) / 1e9
+        res[name] = {"trees": B, "us": ms * 1e3, "trees_per_s": B / (ms / 1e3),
+                     "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak}}
+        del t, p, out
+    torch.cuda.empty_cache()
+    return res
+
+
 def router_bench(ev, gen, torch, stream):
     """A8: router logits GEMM (tcgen05) + TopK + union on the C2/C3/C4 shapes.
     Bytes = L·(T·d + E·d)·2, flops = 2·L·T·d·E with T = packed kept rows (Σ k*)."""
@@ -737,6 +769,10 @@ def run_native(args, rank, world, local_rank):
             result["router"] = router_bench(ev, gen, torch, stream)
         except Exception as e:  # pragma: no cover
             result["router"] = {"error": repr(e)}
+        try:
+            result["draft_tree"] = draft_bench(ev, torch, stream)
+        except Exception as e:  # pragma: no cover
+            result["draft_tree"] = {"error": repr(e)}
         try:
             result["dispatch"] = dispatch_bench(ev, gen, torch)
         except Exception as e:  # pragma: no cover

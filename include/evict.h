@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define EVICT_ABI_VERSION 6
+#define EVICT_ABI_VERSION 7
 #define EVICT_MAX_NODES 128   /* N ≤ 128 ⇒ W ≤ 2 mask words */
 #define EVICT_MAX_EXPERTS 256 /* Ling-flash-2.0 has 256 experts */
 #define EVICT_MAX_TOPK 16
@@ -409,6 +409,37 @@ evict_status_t evict_dispatch_create(int32_t n_bodies, const int32_t *lengths, v
                                      evict_dispatch_t *out);
 evict_status_t evict_dispatch_launch(evict_dispatch_t d, void *stream);
 void evict_dispatch_destroy(evict_dispatch_t d);
+
+/* ---------------------------------------------------------------------------
+ * evict_build_draft_tree — NEXT-4 (P2): the EAGLE-style draft tree on the
+ * device (§2.1: the drafter "repeatedly extends a fixed number of
+ * draft tokens … with the same number of tokens at each layer"; the budget
+ * cut keeps "the top-k nodes ranked by cumulative scores").
+ * Per tree b, from the drafter's per-step top-`topk` tables:
+ *   pool = {root}, Score(root) = 1, frontier = [root]
+ *   step s: frontier slot j's children c = 0..topk-1 get parent frontier[j],
+ *     token child_tokens[b][s][j][c], q = child_probs[b][s][j][c],
+ *     Score = fl32(Score(parent)·q) (Eq. 7); the next frontier = the topk
+ *     new nodes with the best (Score desc, creation index asc).  Step 0 uses
+ *     slot 0 (the root) only.
+ *   keep = root + the max_nodes − 1 best pool nodes by (Score desc, creation
+ *     index asc); renumbered by creation index (parent < child, reading Z12).
+ * Inputs (DEVICE): child_tokens int32 / child_probs fp32 [B][steps][topk][topk].
+ * Outputs (DEVICE, [B][N] rows, N = max_nodes): parent (-1 root and pads),
+ *   q (1 root, 0 pads), tokens (-1 root — x_{t+1} comes from the target —
+ *   and pads), n_nodes [B] = min(N, 1 + topk + (steps−1)·topk²), status [B]
+ *   (NULL to skip): BAD_PROB when a read probability is NaN or outside [0,1]
+ *   (that tree's outputs are pads, n = 0).  The rows are a valid
+ *   evict_trees_t (with N % 4 == 0).
+ * Host errors: steps ≥ 1, 1 ≤ topk ≤ 16, 1 ≤ N ≤ 128, pool
+ *   1 + topk + (steps−1)·topk² ≤ EVICT_DRAFT_MAX_POOL.
+ * ------------------------------------------------------------------------- */
+#define EVICT_DRAFT_MAX_POOL 2048
+
+evict_status_t evict_build_draft_tree(int32_t batch, int32_t steps, int32_t topk, int32_t max_nodes,
+                                      const int32_t *child_tokens, const float *child_probs,
+                                      int32_t *parent, float *q, int32_t *tokens, int32_t *n_nodes,
+                                      uint32_t *status, void *stream);
 
 const char *evict_status_string(evict_status_t s);
 int evict_abi_version(void);

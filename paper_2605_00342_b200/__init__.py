@@ -105,6 +105,7 @@ def lib():
             L.evict_router_union.argtypes = [vp] * 9
             L.evict_verify_sample.argtypes = [vp, vp, i32, ctypes.c_int64, i32] + [vp] * 7
             L.evict_dispatch_create.argtypes = [i32, vp, vp, vp, vp, vp, vp]
+            L.evict_build_draft_tree.argtypes = [i32] * 4 + [vp] * 7
             L.evict_dispatch_launch.argtypes = [vp, vp]
             L.evict_dispatch_destroy.argtypes = [vp]
             L.evict_dispatch_destroy.restype = None
@@ -117,7 +118,7 @@ def lib():
                       "evict_select_build_union", "evict_router_union", "evict_batch_stats",
                       "evict_select_policy", "evict_select_build_union_policy", "evict_union_curve",
                       "evict_profile_cost", "evict_verify_sample", "evict_dispatch_create",
-                      "evict_dispatch_launch"):
+                      "evict_dispatch_launch", "evict_build_draft_tree"):
                 getattr(L, f).restype = ctypes.c_int
             _lib = L
     return _lib
@@ -393,6 +394,29 @@ def evict_verify_sample(verify_offsets, next_token, next_sibling, retrieve_index
                                    _p(out["accept_len"]), _p(out["accepted_slots"]), _p(out["bonus_token"]),
                                    _p(out["status"]), _stream(stream))
     _check(rc, "evict_verify_sample")
+    return out
+
+
+# ----------------------------------------------------------------- draft-tree builder (NEXT-4, P2)
+def evict_build_draft_tree(child_tokens, child_probs, max_nodes, out=None, stream=None):
+    """child_tokens int32 / child_probs fp32 CUDA [B][steps][topk][topk] → dict(parent, q, tokens
+    [B][max_nodes], n_nodes [B], status [B]) — a ready evict_trees_t batch."""
+    B, S, K1, K2 = child_tokens.shape
+    assert K1 == K2 and child_probs.shape == child_tokens.shape
+    assert child_tokens.dtype == torch.int32 and child_probs.dtype == torch.float32
+    assert child_tokens.is_contiguous() and child_probs.is_contiguous()
+    dev = child_tokens.device
+    N = int(max_nodes)
+    if out is None:
+        out = dict(parent=torch.empty((B, N), dtype=torch.int32, device=dev),
+                   q=torch.empty((B, N), dtype=torch.float32, device=dev),
+                   tokens=torch.empty((B, N), dtype=torch.int32, device=dev),
+                   n_nodes=torch.empty(B, dtype=torch.int32, device=dev),
+                   status=torch.empty(B, dtype=torch.int32, device=dev))
+    rc = lib().evict_build_draft_tree(B, S, K1, N, _p(child_tokens), _p(child_probs), _p(out["parent"]),
+                                      _p(out["q"]), _p(out["tokens"]), _p(out["n_nodes"]), _p(out["status"]),
+                                      _stream(stream))
+    _check(rc, "evict_build_draft_tree")
     return out
 
 

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(ev.LIB_PATH)
     missing = [f for f in declared_functions() if not hasattr(lib, f)]
     assert not missing, missing
-    assert lib.evict_abi_version() == 6
+    assert lib.evict_abi_version() == 7
     lib.evict_workspace_bytes.restype = ctypes.c_size_t
     assert lib.evict_workspace_bytes(64) == 8 * (1 + 16)   # one state word per 4-tree warp tile
 
