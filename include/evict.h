@@ -431,7 +431,7 @@ void evict_dispatch_destroy(evict_dispatch_t d);
  *   (NULL to skip): BAD_PROB when a read probability is NaN or outside [0,1]
  *   (that tree's outputs are pads, n = 0).  The rows are a valid
  *   evict_trees_t (with N % 4 == 0).
- * Host errors: steps ≥ 1, 1 ≤ topk ≤ 16, 1 ≤ N ≤ 128, pool
+ * Host errors: 1 ≤ steps ≤ 16, 1 ≤ topk ≤ 16, 1 ≤ N ≤ 128, pool
  *   1 + topk + (steps−1)·topk² ≤ EVICT_DRAFT_MAX_POOL.
  * ------------------------------------------------------------------------- */
 #define EVICT_DRAFT_MAX_POOL 2048
