@@ -329,7 +329,7 @@ __host__ __device__ inline size_t fused_smem_bytes(int L, int E, bool flags)
            + (size_t)kWarps * grp::GShape<G>::TPW * grp::GShape<G>::NMAX; // ranks (order row)
 }
 
-// LEAN: the serving / bench configuration (u8 top-8 ids, E = 128, no order row, no
+// LEAN: the serving / bench configuration (u8 top-8 ids, E = 128 or 128 < E ≤ 256, no order row, no
 // union bit rows, no histogram) compiled without the other paths — with warps in
 // different phases the full kernel's code footprint thrashes the instruction cache.
 template <int NPL, int IDF, int KT, int EW, int CL, bool LEAN = false>
@@ -443,10 +443,14 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 if (b >= tr.batch) break;
                 EmitRec<G> &er = rec[slot];
                 uint32_t st = er.status;
-                if constexpr (LEAN)
+                if constexpr (LEAN && EW == 2)
                     tree_union_flags64<1, CL, true, false>(st, er.klist, er.k, b, N, L, E, rt.ids, wscr,
                                                            out.union_count, out.union_total, nullptr,
                                                            &epoch);
+                else if constexpr (LEAN)   // 128 < E ≤ 256 (Ling-flash-2.0): 32-byte expert rows
+                    tree_union_flags64<1, CL, false, false, true>(st, er.klist, er.k, b, N, L, E, rt.ids, wscr,
+                                                                  out.union_count, out.union_total, nullptr,
+                                                                  &epoch);
                 else
                     tree_union<NPL, IDF, KT, EW, CL>(st, er.klist, er.k, b, N, L, rt.top_k, E, rt.id_format,
                                                      rt.ids, wscr, Epad, out.union_count, out.union_total,
@@ -627,8 +631,9 @@ struct FusedLauncher {
                               int ntiles, cudaStream_t s)
     {
         auto kern = k_fused<NPL, IDF, KT, EW, CL, false>;
-        if constexpr (IDF == 1 && EW == 2) {
-            if (rt->num_experts == 128 && !o->order && !o->union_bits && !o->expert_hist && o->union_count)
+        if constexpr (IDF == 1 && (EW == 2 || EW == 4)) {
+            const bool shape = EW == 2 ? rt->num_experts == 128 : rt->num_experts > 128;
+            if (shape && !o->order && !o->union_bits && !o->expert_hist && o->union_count)
                 kern = k_fused<NPL, IDF, KT, EW, CL, true>;
         }
         constexpr int G = NPL == 2 ? 8 : 16;

@@ -1074,7 +1074,9 @@ __device__ __forceinline__ void tree_union_flags(uint32_t &status, const uint8_t
 // (R · 256 · 16 bytes) for E > 128.
 __host__ __device__ inline int union_flag_bytes(int L, int E)
 {
-    return E <= 128 ? 8192 : 16 * 256 * ((2 * L + 31) / 32);
+    (void)L;
+    (void)E;
+    return 8192;   // E ≤ 128: 128 experts × 64 layer bytes; E ≤ 256: 256 experts × 32 layer bytes
 }
 
 // Top-K ids (u8 or i32, E ≤ 128) via an expert-major shared-memory flag block
@@ -1112,7 +1114,10 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr)
     return v;
 }
 
-template <int IDF, int R, bool E128, bool BITS>
+// W256 (128 < E ≤ 256, Ling-flash-2.0): the same scheme with 32-byte expert rows — passes
+// of 32 layers, flag(l, e) at byte e·32 + 4·(l%8) + (l/8)%4; the read-back widens the byte
+// sums to 16-bit lanes before the cross-lane reduction (a layer can hold all 256 experts).
+template <int IDF, int R, bool E128, bool BITS, bool W256 = false>
 __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8_t *__restrict__ klist, int k,
                                                    int b, int N, int L, int E, const void *__restrict__ ids,
                                                    uint8_t *flags, int32_t *__restrict__ union_count,
@@ -1120,7 +1125,9 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                                                    uint64_t *__restrict__ union_bits, int *epoch = nullptr)
 {
     static_assert(IDF == 1 || IDF == 4, "flag union takes u8 or i32 ids");
-    constexpr int PASSES = (R + 3) / 4;
+    constexpr int RPP = W256 ? 2 : 4;                  // 16-layer rounds per pass
+    constexpr int PASSES = (R + RPP - 1) / RPP;
+    constexpr int ESH = W256 ? 5 : 6;                  // log2 bytes per expert row
     // Marker mode (single pass, no bit rows, caller keeps `epoch`): tree t stores the
     // byte 1 << (t mod 4) and counts only that bit, so the block is cleared once per 4
     // trees instead of after every tree (a byte holds its last writer's marker; the 4
@@ -1128,13 +1135,17 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
     const bool mark = PASSES == 1 && !BITS && epoch != nullptr;
     const int ep = mark ? *epoch : 0;
     const uint32_t marker = 1u << ep;
-    constexpr int RP = R < 4 ? R : 4;                  // rounds per pass
+    constexpr int RP = R < RPP ? R : RPP;              // rounds per pass
     constexpr int U = IDF == 1 ? 4 : 1;                // nodes per load batch (i32 rows are 4x wider)
     const int lane = lane_id();
     const int S = 2 * L;
     const uint32_t row = (uint32_t)S;                  // 4-id units per node row
     const uint32_t fbase = (uint32_t)__cvta_generic_to_shared(flags);
-    const uint32_t lbase = fbase + 4u * (uint32_t)(lane >> 1);   // + e·64 + round byte
+    // + (e << ESH) + round byte: layer 16c + j' (j' = lane/2) sits at byte 4·(l%16) + l/16 (E ≤ 128)
+    // or 4·(l%8) + l/8 (W256)
+    const uint32_t jp = (uint32_t)(lane >> 1);
+    const uint32_t lbase = W256 ? fbase + 4u * (jp & 7u) + (jp >> 3) : fbase + 4u * jp;
+    constexpr uint32_t CSTEP = W256 ? 2u : 1u;         // byte step of one round
     uint32_t bad = 0;
     const bool run = status == 0;
     int tot = 0;
@@ -1146,8 +1157,8 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
             // (the read-back still clears it).
             // this lane's first unit of the pass in the tree's node-row block; a node adds
             // node·row units (32-bit: node < 128, row ≤ 256) and a round 32 units
-            const uint32_t *lane_u32 = reinterpret_cast<const uint32_t *>(ids) + (size_t)b * N * row + lane + 128 * pass;
-            const int4 *lane_i4 = reinterpret_cast<const int4 *>(ids) + (size_t)b * N * row + lane + 128 * pass;
+            const uint32_t *lane_u32 = reinterpret_cast<const uint32_t *>(ids) + (size_t)b * N * row + lane + 32 * RPP * pass;
+            const int4 *lane_i4 = reinterpret_cast<const int4 *>(ids) + (size_t)b * N * row + lane + 32 * RPP * pass;
             for (int j0 = 0; j0 < k; j0 += U) {
                 uint32_t v[U][RP][IDF];
 #pragma unroll
@@ -1155,7 +1166,7 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                     const uint32_t node = klist[min(j0 + u, k - 1)];
 #pragma unroll
                     for (int cc = 0; cc < RP; cc++) {
-                        const bool ok = lane + 32 * (4 * pass + cc) < S;
+                        const bool ok = lane + 32 * (RPP * pass + cc) < S;
                         if constexpr (IDF == 1) {
                             const uint32_t *rp = reinterpret_cast<const uint32_t *>(
                                 reinterpret_cast<const char *>(lane_u32) + node * (4u * row));
@@ -1175,22 +1186,22 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                     for (int cc = 0; cc < RP; cc++) {
                         if constexpr (IDF == 1) {
                             const uint32_t wv = v[u][cc][0];
-                            const uint32_t wm = wv & 0x7F7F7F7Fu;
+                            const uint32_t wm = W256 ? wv : wv & 0x7F7F7F7Fu;
                             if constexpr (E128) {
                                 bad |= wv & 0x80808080u;
                             } else {
-#pragma unroll
-                                for (int qb = 0; qb < 4; qb++) bad |= ((wv >> (8 * qb)) & 0xffu) >= (uint32_t)E;
+                                // SIMD byte compare (E ≤ 255); every u8 id is valid when E = 256
+                                if (E < 256) bad |= __vcmpgeu4(wv, 0x01010101u * (uint32_t)E);
                             }
 #pragma unroll
                             for (int qb = 0; qb < 4; qb++)
-                                sts_u8((__byte_perm(wm, 0, 0x4440 | qb) << 6) + (lbase + cc), marker);
+                                sts_u8((__byte_perm(wm, 0, 0x4440 | qb) << ESH) + (lbase + CSTEP * cc), marker);
                         } else {
 #pragma unroll
                             for (int qb = 0; qb < 4; qb++) {
                                 const uint32_t e = v[u][cc][qb];
                                 bad |= e >= (uint32_t)E;
-                                sts_u8(((e & 127u) << 6) + (lbase + cc), marker);
+                                sts_u8(((e & (W256 ? 255u : 127u)) << ESH) + (lbase + CSTEP * cc), marker);
                             }
                         }
                     }
@@ -1202,17 +1213,15 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                 // per-layer bit rows (test configuration only): lane = layer of this pass
                 const int EWr = (E + 63) >> 6;
 #pragma unroll 1
-                for (int li = lane; li < 64; li += 32) {
-                    const int l = 64 * pass + li;
+                for (int li = lane; li < 16 * RPP; li += 32) {
+                    const int l = 16 * RPP * pass + li;
                     if (l >= L) break;
-                    const uint32_t fl = fbase + 4u * (uint32_t)(li & 15) + (uint32_t)(li >> 4);
-                    uint64_t lo = 0ull, hi = 0ull;
-                    for (int e = 0; e < E; e++) {
-                        const uint64_t bit = lds_u8(fl + ((uint32_t)e << 6)) ? 1ull << (e & 63) : 0ull;
-                        if (e < 64) lo |= bit; else hi |= bit;
-                    }
-                    union_bits[((size_t)b * L + l) * EWr] = lo;
-                    if (EWr > 1) union_bits[((size_t)b * L + l) * EWr + 1] = hi;
+                    const uint32_t fl = W256 ? fbase + 4u * (uint32_t)(li & 7) + (uint32_t)(li >> 3)
+                                             : fbase + 4u * (uint32_t)(li & 15) + (uint32_t)(li >> 4);
+                    uint64_t wd[4] = {0ull, 0ull, 0ull, 0ull};
+                    for (int e = 0; e < E; e++)
+                        if (lds_u8(fl + ((uint32_t)e << ESH))) wd[e >> 6] |= 1ull << (e & 63);
+                    for (int h = 0; h < EWr; h++) union_bits[((size_t)b * L + l) * EWr + h] = wd[h];
                 }
                 __syncwarp();
             }
@@ -1238,6 +1247,29 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                     sts_v4_zero(fw + 512u * i);
                 }
             }
+            if constexpr (W256) {
+                // lane reads expert rows e = lane/2 + 16i, word quad h = lane&1 (words 4h..4h+3 =
+                // layers l%8); the cross-lane sum spans 256 experts, so widen bytes to 16-bit lanes
+                uint32_t lo[4] = {a0 & 0x00ff00ffu, a1 & 0x00ff00ffu, a2 & 0x00ff00ffu, a3 & 0x00ff00ffu};
+                uint32_t hi[4] = {(a0 >> 8) & 0x00ff00ffu, (a1 >> 8) & 0x00ff00ffu, (a2 >> 8) & 0x00ff00ffu,
+                                  (a3 >> 8) & 0x00ff00ffu};
+#pragma unroll
+                for (int o = 2; o < 32; o <<= 1)
+#pragma unroll
+                    for (int mm = 0; mm < 4; mm++) {
+                        lo[mm] += __shfl_xor_sync(kFull, lo[mm], o);
+                        hi[mm] += __shfl_xor_sync(kFull, hi[mm], o);
+                    }
+                const int u = lane >> 1, m = u & 3, beta = u >> 2;     // layer 8β + 4h + m
+                const uint32_t wsel = (beta & 1) ? (m == 0 ? hi[0] : m == 1 ? hi[1] : m == 2 ? hi[2] : hi[3])
+                                                 : (m == 0 ? lo[0] : m == 1 ? lo[1] : m == 2 ? lo[2] : lo[3]);
+                const int l = 32 * pass + 8 * beta + 4 * (lane & 1) + m;
+                if (l < L) {
+                    const int cnt = (int)((wsel >> (16 * (beta >> 1))) & 0xffffu);
+                    union_count[(size_t)b * L + l] = cnt;
+                    tot += cnt;
+                }
+            } else {
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
                 a0 += __shfl_xor_sync(kFull, a0, o);
@@ -1256,6 +1288,7 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                     union_count[(size_t)b * L + l] = cnt;
                     tot += cnt;
                 }
+            }
             }
         }
         __syncwarp();
@@ -1302,12 +1335,12 @@ __device__ __forceinline__ void tree_union(uint32_t &status, const uint8_t *__re
                     else tree_union_flags64<IDF, R, false, true>(status, klist, k, b, N, L, E, ids, flags,
                                                                  union_count, union_total, union_bits);
                 }
-            } else if (union_bits == nullptr) {
-                tree_union_flags<NPL, IDF, R, false, false>(status, klist, k, b, N, L, E, ids, flags, Epad,
-                                                            union_count, union_total, nullptr);
+            } else if (union_bits == nullptr) {   // 128 < E ≤ 256: 32-byte expert rows
+                tree_union_flags64<IDF, R, false, false, true>(status, klist, k, b, N, L, E, ids, flags,
+                                                               union_count, union_total, nullptr);
             } else {
-                tree_union_flags<NPL, IDF, R, false, true>(status, klist, k, b, N, L, E, ids, flags, Epad,
-                                                           union_count, union_total, union_bits);
+                tree_union_flags64<IDF, R, false, true, true>(status, klist, k, b, N, L, E, ids, flags,
+                                                              union_count, union_total, union_bits);
             }
         } else {
             tree_union_generic<NPL, IDF, KT, EW, (R + 1) / 2>(status, klist, k, b, N, L, K, E, idb, ids,

@@ -414,3 +414,22 @@ def test_policy_rejects_bad_arguments(ev):
     for bad in (("coverage", 0.0), ("coverage", 1.5), ("coverage", float("nan")), ("fixed", 0)):
         with pytest.raises(ev.EvictError):
             ev.evict_select(P, Q, C, policy=bad)
+
+
+@pytest.mark.parametrize("name", ["c2", "ling"])
+def test_fused_lean_path(ev, name):
+    """The serving configuration (u8 top-8 ids, no order row, no bit rows, no histogram) runs the
+    LEAN instantiation with marker-epoch flag blocks — E = 128 and the 256-expert layout."""
+    c = gen.CONFIGS[name]
+    B = 777
+    N, L, E, K = c["N"], c["L"], c["E"], c["K"]
+    P, Q, n = gen.trees(c["seed"] + 3, B, N, c["steps"], c["topk"])
+    n[::5] = np.maximum(1, n[::5] // 3)
+    cost = gen.cost_table(N)
+    ids = gen.routing(c["seed"] + 1, B, N, L, E, K)
+    g = npy(ev.evict_select_build_union(T(P), T(Q), T(cost), T(ids), E, n_nodes=T(n)))
+    o = oracle.select(P, Q, cost, n_nodes=n, threads=8)
+    res, msgs = compare_select(o, g, n_nodes=n)
+    assert not msgs, msgs[:5]
+    ou = oracle.expert_union(downstream_keep(o, g), ids, E, n_nodes=n, threads=8)
+    assert not compare_union(ou, {k: v for k, v in g.items() if k in ("union_count", "union_total")})
