@@ -580,8 +580,8 @@ def draft_bench(ev, torch, stream):
         ach = byt / (ms / 1e3) / 1e9
         res[name] = {"trees": B, "us": ms * 1e3, "trees_per_s": B / (ms / 1e3),
                      "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak},
-                     "note": "issue-bound, not HBM-bound: ~37K warp instructions per tree, 76% issue slots "
-                             "(profiles/r01_draft_v3_ncu.md)"}
+                     "note": "issue-bound, not HBM-bound: warp-per-tree kernel (batch >= 4 SMs) ~12K warp "
+                             "instructions per tree (profiles/r01_draft_v4_ncu.md); CTA-per-tree below that"}
         del t, p, out
     torch.cuda.empty_cache()
     return res

@@ -32,6 +32,10 @@ def _compare(o, g):
     (1, 1, 8, 10),        # top-1 chain
     (9, 15, 128, 8),      # pool 1 + 15 + 8·225 = 1816 (near the 2048 limit)
     (2, 3, 100, 20),      # budget above the pool: no cut
+    (6, 10, 60, 1500),    # ≥ 4·SMs trees: the warp-per-tree kernel (C2 shape)
+    (4, 8, 32, 700),      # warp-per-tree, paper shape
+    (3, 16, 128, 700),    # warp-per-tree, 256 candidates per step (8 keys per lane)
+    (5, 2, 16, 800),      # warp-per-tree, tiny steps (1 key per lane)
 ])
 def test_builder_matches_oracle(steps, topk, N, B):
     tok, pr = drafter_tables(steps * 100 + topk, B, steps, topk)
