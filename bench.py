@@ -307,6 +307,17 @@ def latency_b64(ev, torch, gen, N=60, steps=6, topk=10, seed=4, replays=2000):
             e1.record(s)
         e1.synchronize()
         out[f"{name}_b64_n{N}_us"] = e0.elapsed_time(e1) * 1e3 / replays
+        # per-replay device times (SURVEY §8(d) latency): p50 / p99 over 1000 replays
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(1000)]
+        with torch.cuda.stream(s):
+            for a, b in evs:
+                a.record(s)
+                g.replay()
+                b.record(s)
+        s.synchronize()
+        t = np.sort([a.elapsed_time(b) * 1e3 for a, b in evs])
+        out[f"{name}_b64_n{N}_p50_us"] = float(t[len(t) // 2])
+        out[f"{name}_b64_n{N}_p99_us"] = float(t[int(len(t) * 0.99)])
     return out
 
 
