@@ -17,8 +17,9 @@ def _step(ev, torch, bufs, s):
     d = ev.evict_build_draft_tree(bufs["ctok"], bufs["cprob"], bufs["N"], out=bufs["tree"], stream=s)
     f = ev.evict_select_build_union(d["parent"], d["q"], bufs["cost"], bufs["ids"], bufs["E"],
                                     n_nodes=d["n_nodes"], buffers=bufs["fused"], stream=s)
-    # stand-in for the target's verify pass: its next-token rows in packed verify order
-    ri = f["retrieve_index"].clamp(min=0).long()
+    # stand-in for the target's verify pass: its next-token rows in packed verify order (rows past
+    # the step's T = verify_offsets[B] are capacity, not written by the library: clamp their index)
+    ri = f["retrieve_index"].clamp(0, bufs["node_probs"].shape[0] - 1).long()
     torch.index_select(bufs["node_probs"], 0, ri, out=bufs["probs"])
     return ev.evict_verify_sample(f["verify_offsets"], f["next_token"], f["next_sibling"], f["retrieve_index"],
                                   d["tokens"], bufs["probs"], u_accept=bufs["ua"], u_bonus=bufs["ub"],
