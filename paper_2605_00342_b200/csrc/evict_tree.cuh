@@ -1152,9 +1152,9 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
 #pragma unroll 1
     for (int pass = 0; pass < PASSES; pass++) {
         if (run) {
-            // No store guards: a batch past k re-reads node k-1 (the union is idempotent) and
-            // a slot past 2L stores e = 0 into a layer ≥ L, whose byte is never counted
-            // (the read-back still clears it).
+            // A batch past k re-reads node k-1 (cheap L1 hits) but stores nothing for it; a slot
+            // past 2L stores e = 0 into a layer ≥ L, whose byte is never counted (the read-back
+            // still clears it).
             // this lane's first unit of the pass in the tree's node-row block; a node adds
             // node·row units (32-bit: node < 128, row ≤ 256) and a round 32 units
             const uint32_t *lane_u32 = reinterpret_cast<const uint32_t *>(ids) + (size_t)b * N * row + lane + 32 * RPP * pass;
@@ -1181,7 +1181,8 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < U; u++)
+                for (int u = 0; u < U; u++) {
+                    if (j0 + u >= k) break;    // warp-uniform: a batch's tail re-read of node k-1 stores nothing
 #pragma unroll
                     for (int cc = 0; cc < RP; cc++) {
                         if constexpr (IDF == 1) {
@@ -1205,6 +1206,7 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                             }
                         }
                     }
+                }
             }
         }
         __syncwarp();
