@@ -298,18 +298,20 @@ def test_fused_equals_oracle(ev, name, fmt, with_order):
 
 # ------------------------------------------------------------------ stats
 def test_batch_stats(ev):
+    """Both sides aggregate the same per-tree inputs, produced by the oracle (select + union)."""
     B, N, L, E, K = 5000, 60, 48, 128, 8
     P, Q, n = gen.trees(3, B, N, 6, 10)
     Q[17, 5] = 2.0                                           # one bad tree
     cost = gen.cost_table(N)
     ids = gen.routing(3, B, N, L, E, K)
-    g = ev.evict_select_build_union(T(P), T(Q), T(cost), T(ids), E, n_nodes=T(n))
-    s, d = ev.evict_batch_stats(g["k_star"], g["e_hat"], g["utility"], g["union_count"],
-                                g["status"], N, n_nodes=T(n))
-    gg = npy(g)
-    so, do = oracle.batch_stats(N, L, gg["k_star"], gg["e_hat"].astype(np.float64),
-                                gg["utility"].astype(np.float64), gg["union_count"],
-                                gg["status"].astype(np.uint32), n_nodes=n)
+    o = oracle.select(P, Q, cost, n_nodes=n, threads=8)
+    u = oracle.expert_union(o["keep_bits"], ids, E, n_nodes=n, threads=8)
+    e_hat = o["e_hat"].astype(np.float32)                    # the kernel's input precision
+    util = o["utility"].astype(np.float32)
+    s, d = ev.evict_batch_stats(T(o["k_star"]), T(e_hat), T(util), T(u["union_count"]),
+                                T(o["status"].view(np.int32)), N, n_nodes=T(n))
+    so, do = oracle.batch_stats(N, L, o["k_star"], e_hat.astype(np.float64), util.astype(np.float64),
+                                u["union_count"], o["status"], n_nodes=n)
     assert (s.cpu().numpy() == so).all()
     assert np.allclose(d.cpu().numpy(), do, rtol=1e-9)
     assert so[4] == 1

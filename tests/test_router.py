@@ -57,9 +57,10 @@ def test_router_integer_inputs_bit_exact(ev, B, N, steps, topk, L, d, K, E, hint
     o = oracle.router_union(keep, h, w, K, threads=8)
     gg = {k: v.cpu().numpy() for k, v in g.items()}
     assert not compare_union(o, gg)
-    # per-row TopK ids, in rank order
-    T = int(b["verify_offsets"][-1])
-    ridx = b["retrieve_index"].cpu().numpy()
+    # per-row TopK ids, in rank order (rows located through the oracle's verify layout)
+    ob = oracle.build_verify_tree(P, keep, n_nodes=n)
+    T = int(ob["verify_offsets"][-1])
+    ridx = ob["retrieve_index"]
     rows = np.random.default_rng(0).choice(T, min(T, 40), replace=False)
     for l in range(L):
         for r in rows:
