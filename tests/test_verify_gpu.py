@@ -196,9 +196,9 @@ def test_parity_threshold_on_a_cdf_boundary(exact):
 @pytest.mark.parametrize("B", [150, 300, 600, 1200, 2400])
 @pytest.mark.parametrize("greedy", [False, True])
 def test_parity_cluster_sizes(B, greedy):
-    """Batch sizes that select 4-, 2- and 1-CTA clusters per tree for sampling and 1 for greedy
-    (the launch splits a tree's row over a thread-block cluster until the grid covers 16·SMs
-    CTAs for sampling, 4·SMs for greedy); batches ≤ 64 elsewhere use 8."""
+    """Batch sizes that select 4-, 2- and 1-CTA clusters per tree (the launch splits a tree's
+    row over a thread-block cluster until the grid covers 4·SMs CTAs); batches ≤ 64 elsewhere
+    use 8."""
     V = 300
     P, Q, n, kb, off, tok, probs, ua, ub = _case(17, B, 60, V, keep="all")
     mode = ov.GREEDY if greedy else ov.SAMPLE
