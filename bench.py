@@ -599,8 +599,9 @@ def draft_bench(ev, torch, stream):
 
 
 def router_bench(ev, gen, torch, stream):
-    """A8: router logits GEMM (tcgen05) + TopK + union on the C2/C3/C4 shapes.
-    Bytes = L·(T·d + E·d)·2, flops = 2·L·T·d·E with T = packed kept rows (Σ k*)."""
+    """A8: router logits GEMM (tcgen05) + TopK + union on the C2/C3/C4 shapes and
+    the Ling-flash-2.0 shape.  Bytes = L·(T·d + E·d)·2, flops = 2·L·T·d·E with T = packed kept
+    rows (Σ k*).  µs per call by CUDA-graph replay (memset + router + finalize)."""
     import numpy as np
     res = {}
     peaks_ = peaks()
@@ -619,15 +620,26 @@ def router_bench(ev, gen, torch, stream):
         w = gen.wgate_cuda(12, L, E, d, mode=1, scale_log2=-5)
         T = int(b["verify_offsets"][-1])
         rc = ev.RouterCall(b["verify_offsets"], b["retrieve_index"], h, w, TOP_K, B, Nn, max_rows=T)
-        for _ in range(3):
-            rc(stream)
-        reps = 50
+        gs = torch.cuda.Stream()
+        with torch.cuda.stream(gs):
+            for _ in range(3):
+                rc(gs)
+            gs.synchronize()
+            # the call (bitset clear + router + finalize) captured once, as in a serving graph
+            # (PAPER.md:198-204); replays are timed, so launch gaps are not counted
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=gs):
+                rc(gs)
+            for _ in range(5):
+                graph.replay()
+        reps = 200
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(reps):
-            rc(stream)
-        e1.record(stream)
+        with torch.cuda.stream(gs):
+            e0.record(gs)
+            for _ in range(reps):
+                graph.replay()
+            e1.record(gs)
         e1.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / reps
         byt = L * (T * d + E * d) * 2
