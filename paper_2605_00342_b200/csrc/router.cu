@@ -104,6 +104,14 @@ __device__ __forceinline__ uint32_t mapa_cluster(uint32_t addr, uint32_t rank)
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
     return r;
 }
+__device__ __forceinline__ float4 ld_cluster_v4(uint32_t addr)
+{
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ float ld_cluster_f32(uint32_t addr)
 {
     float v;
@@ -491,14 +499,24 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
 #pragma unroll 1
             for (int zz = 1; zz < S; zz++) {
                 const uint32_t rem = mapa_cluster(mine, (uint32_t)zz);
+                // 16-byte DSMEM loads over the flat block, two per thread in flight; the same
+                // per-element order (split 0 + 1 + …) as a scalar loop
+                float4 *lg4 = reinterpret_cast<float4 *>(base);
+                const int nf4 = nf >> 2;
                 int f = threadIdx.x;
 #pragma unroll 1
-                for (; f + 3 * BM < nf; f += 4 * BM) {
-                    const float a0 = ld_cluster_f32(rem + 4u * f), a1 = ld_cluster_f32(rem + 4u * (f + BM));
-                    const float a2 = ld_cluster_f32(rem + 4u * (f + 2 * BM)), a3 = ld_cluster_f32(rem + 4u * (f + 3 * BM));
-                    lgf[f] += a0; lgf[f + BM] += a1; lgf[f + 2 * BM] += a2; lgf[f + 3 * BM] += a3;
+                for (; f + BM < nf4; f += 2 * BM) {
+                    const float4 a = ld_cluster_v4(rem + 16u * f), c = ld_cluster_v4(rem + 16u * (f + BM));
+                    float4 &x = lg4[f], &y = lg4[f + BM];
+                    x.x += a.x; x.y += a.y; x.z += a.z; x.w += a.w;
+                    y.x += c.x; y.y += c.y; y.z += c.z; y.w += c.w;
                 }
-                for (; f < nf; f += BM) lgf[f] += ld_cluster_f32(rem + 4u * f);
+                for (; f < nf4; f += BM) {
+                    const float4 a = ld_cluster_v4(rem + 16u * f);
+                    float4 &x = lg4[f];
+                    x.x += a.x; x.y += a.y; x.z += a.z; x.w += a.w;
+                }
+                for (int t = 4 * nf4 + threadIdx.x; t < nf; t += BM) lgf[t] += ld_cluster_f32(rem + 4u * t);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");   // warps 0–3 only
         }
