@@ -601,7 +601,8 @@ def draft_bench(ev, torch, stream):
 def router_bench(ev, gen, torch, stream):
     """A8: router logits GEMM (tcgen05) + TopK + union on the C2/C3/C4 shapes and
     the Ling-flash-2.0 shape.  Bytes = L·(T·d + E·d)·2, flops = 2·L·T·d·E with T = packed kept
-    rows (Σ k*).  µs per call by CUDA-graph replay (memset + router + finalize)."""
+    rows (Σ k*).  µs per call: median over 100 CUDA-graph replays (memset + router + finalize),
+    each after a 256 MB write that evicts the inputs from L2."""
     import numpy as np
     res = {}
     peaks_ = peaks()
@@ -632,16 +633,21 @@ def router_bench(ev, gen, torch, stream):
                 rc(gs)
             for _ in range(5):
                 graph.replay()
-        reps = 200
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # cold L2: W_g + the kept hidden rows (25–95 MB) would otherwise stay resident in the
+        # 126 MB L2 across replays; a 256 MB write evicts them before every timed replay
+        reps = 100
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
         torch.cuda.synchronize()
         with torch.cuda.stream(gs):
-            e0.record(gs)
-            for _ in range(reps):
+            for a, c in evs:
+                flush.fill_(1)
+                a.record(gs)
                 graph.replay()
-            e1.record(gs)
-        e1.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / reps
+                c.record(gs)
+        gs.synchronize()
+        us = float(np.median([a.elapsed_time(c) for a, c in evs])) * 1e3
+        del flush
         byt = L * (T * d + E * d) * 2
         fl = 2.0 * L * T * d * E
         res[name] = {"B": B, "N": Nn, "L": L, "d": d, "E": E, "rows": T, "us": us,

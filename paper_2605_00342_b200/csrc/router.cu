@@ -203,11 +203,12 @@ __device__ __forceinline__ Bits<NE> topk_scan(const float *lg, int K, bool valid
     int bi[KL];
     const float ninf = -__int_as_float(0x7f800000);
     float gmin = __int_as_float(0x7f800000);
+    const float4 *lg4 = reinterpret_cast<const float4 *>(lg);   // 16-byte aligned rows
 #pragma unroll 1
     for (int g = 0; g < BN / 16; g++) {
-        float m = lg[g * 16];
-#pragma unroll
-        for (int i = 1; i < 16; i++) m = fmaxf(m, lg[g * 16 + i]);
+        const float4 a = lg4[4 * g], b = lg4[4 * g + 1], c = lg4[4 * g + 2], d = lg4[4 * g + 3];
+        const float m = fmaxf(fmaxf(fmaxf(fmaxf(a.x, a.y), fmaxf(a.z, a.w)), fmaxf(fmaxf(b.x, b.y), fmaxf(b.z, b.w))),
+                              fmaxf(fmaxf(fmaxf(c.x, c.y), fmaxf(c.z, c.w)), fmaxf(fmaxf(d.x, d.y), fmaxf(d.z, d.w))));
         gmin = fminf(gmin, m);
     }
     // valid as a lower bound for the K-th largest only when K ≤ BN/16 groups
@@ -230,9 +231,14 @@ __device__ __forceinline__ Bits<NE> topk_scan(const float *lg, int K, bool valid
     for (int c = 0; c < BN; c += 32) {
         uint32_t cand = 0u;
 #pragma unroll
-        for (int i = 0; i < 32; i++) {
-            const float v = lg[c + i];
-            cand |= (v >= thr && (filled < K || v > kth)) ? (1u << i) : 0u;
+        for (int q = 0; q < 8; q++) {
+            const float4 x = lg4[(c >> 2) + q];
+            const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const float v = xv[j];
+                cand |= (v >= thr && (filled < K || v > kth)) ? (1u << (4 * q + j)) : 0u;
+            }
         }
         while (cand) {
             const int i = c + __ffs(cand) - 1;
@@ -344,8 +350,9 @@ __global__ void __launch_bounds__(THREADS, STAGES <= 3 ? 2 : 1)
 k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap hmap, Params p)
 {
     constexpr int BN = NE, EW = NE / 64;
+    constexpr int LS = BN + 4;   // staged logit row stride (floats): 16-byte rows, conflict-free float4 phases
     constexpr int B_BYTES = b_bytes<NE>(), STAGE_BYTES = stage_bytes<NE>();
-    static_assert(BM * (BN + 1) * 4 <= STAGES * STAGE_BYTES, "logit staging must fit the operand ring");
+    static_assert(BM * LS * 4 <= STAGES * STAGE_BYTES, "logit staging must fit the operand ring");
     extern __shared__ uint8_t smem_raw[];
     const int T = __ldg(p.verify_offsets + p.B);
     const int m0 = blockIdx.x * BM;
@@ -367,7 +374,10 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
     // sparse tiles gather their few hidden rows with TMA (gather4, one issuing thread);
     // dense tiles use 128 cp.async producers (one TMA thread would serialise 32 gathers)
     const bool sparse = nrow <= 32;
-    if (tr0 && threadIdx.x == 0) p.trace[250] = gtimer();
+    if (tr0 && threadIdx.x == 0) {
+        p.trace[250] = gtimer();
+        p.trace[251] = p.splits;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(full0 + 8 * s, sparse ? 1 : NPROD + 1);
@@ -395,7 +405,7 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
     const int NKB = kb1 - kb0;
     const size_t BNrows = (size_t)p.B * p.N;
     const int row = warp * 32 + lane;         // epilogue row (warps 0–3)
-    float *lg = reinterpret_cast<float *>(base) + (size_t)(row & (BM - 1)) * (BN + 1);
+    float *lg = reinterpret_cast<float *>(base) + (size_t)(row & (BM - 1)) * LS;
 
     if (warp < 4) {
         if (!sparse) {
@@ -424,14 +434,15 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
         mbar_wait(tfull, 0);
         if (tr0 && threadIdx.x == 0) p.trace[193] = gtimer();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        // the operand ring is free now; stride 129 floats: thread t's element i sits in
-        // bank (t + i) % 32
+        // the operand ring is free now; rows of LS = BN + 4 floats written as float4: an 8-thread
+        // phase of a 16-byte store covers 8 distinct 4-bank groups
 #pragma unroll 1
         for (int chunk = 0; chunk < BN / 32; chunk++) {
             float v[32];
             tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + chunk * 32, v);
+            float4 *l4 = reinterpret_cast<float4 *>(lg + chunk * 32);
 #pragma unroll
-            for (int i = 0; i < 32; i++) lg[chunk * 32 + i] = v[i];
+            for (int q = 0; q < 8; q++) l4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
         if (tr0 && threadIdx.x == 0) p.trace[196] = gtimer();
     } else if (warp == 4) {
@@ -486,49 +497,48 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
     }
     if (S > 1) cluster_sync();                // every split's partial is staged
 
-    if (z == 0 && warp < 4) {
-        // ---- leader: ordered sum of the partials (split 0 + 1 + … : deterministic), TopK, union
+    if (warp < 4 && (S > 1 || z == 0)) {
+        // ---- split-K: every split reduces and ranks a contiguous block of ⌈nrow/S⌉ rows (the sum
+        // order per element stays split 0 + 1 + … + S−1: deterministic, as one leader would)
         const int r = m0 + row;
         const bool valid = r < T;
+        int r0 = 0, r1 = nrow;
         if (S > 1) {
-            // the valid rows' partials are one contiguous block: 128 threads stream it
-            // coalesced from each remote split (independent loads, 4 in flight per thread)
-            const int nf = nrow * (BN + 1);
-            float *lgf = reinterpret_cast<float *>(base);
+            const int R = (nrow + S - 1) / S;
+            r0 = min(nrow, z * R);
+            r1 = min(nrow, r0 + R);
+            float4 *lg4 = reinterpret_cast<float4 *>(base);
             const uint32_t mine = smem_u32(base);
+            const int f0 = (r0 * LS) >> 2, f1 = (r1 * LS) >> 2;   // LS % 4 == 0: whole float4 rows
+            uint32_t rem[4];
+#pragma unroll
+            for (int zz = 0; zz < 4; zz++) rem[zz] = zz < S ? mapa_cluster(mine, (uint32_t)zz) : 0u;
 #pragma unroll 1
-            for (int zz = 1; zz < S; zz++) {
-                const uint32_t rem = mapa_cluster(mine, (uint32_t)zz);
-                // 16-byte DSMEM loads over the flat block, two per thread in flight; the same
-                // per-element order (split 0 + 1 + …) as a scalar loop
-                float4 *lg4 = reinterpret_cast<float4 *>(base);
-                const int nf4 = nf >> 2;
-                int f = threadIdx.x;
-#pragma unroll 1
-                for (; f + BM < nf4; f += 2 * BM) {
-                    const float4 a = ld_cluster_v4(rem + 16u * f), c = ld_cluster_v4(rem + 16u * (f + BM));
-                    float4 &x = lg4[f], &y = lg4[f + BM];
-                    x.x += a.x; x.y += a.y; x.z += a.z; x.w += a.w;
-                    y.x += c.x; y.y += c.y; y.z += c.z; y.w += c.w;
-                }
-                for (; f < nf4; f += BM) {
-                    const float4 a = ld_cluster_v4(rem + 16u * f);
-                    float4 &x = lg4[f];
-                    x.x += a.x; x.y += a.y; x.z += a.z; x.w += a.w;
-                }
-                for (int t = 4 * nf4 + threadIdx.x; t < nf; t += BM) lgf[t] += ld_cluster_f32(rem + 4u * t);
+            for (int f = f0 + threadIdx.x; f < f1; f += BM) {
+                float4 acc = ld_cluster_v4(rem[0] + 16u * f);
+                float4 t[3];
+#pragma unroll
+                for (int zz = 1; zz < 4; zz++)
+                    if (zz < S) t[zz - 1] = ld_cluster_v4(rem[zz] + 16u * f);
+#pragma unroll
+                for (int zz = 1; zz < 4; zz++)
+                    if (zz < S) {
+                        acc.x += t[zz - 1].x; acc.y += t[zz - 1].y; acc.z += t[zz - 1].z; acc.w += t[zz - 1].w;
+                    }
+                lg4[f] = acc;   // own rows only: no other split reads this block after the barrier
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");   // warps 0–3 only
         }
-        if (p.dbg_logits && valid)
+        if (p.dbg_logits && valid && row >= r0 && row < r1)
             for (int i = 0; i < BN; i++) p.dbg_logits[((size_t)l * BNrows + r) * BN + i] = lg[i];
-        if (nrow <= 32) {
-            // sparse tile: a warp per row (rows warp, warp + 4, …), one atomic pair per row
+        if (S > 1 || nrow <= 32) {
+            // a warp per row (rows r0 + warp, + 4, …), one atomic group per row: sparse tiles, and
+            // every split's block of a split-K tile
 #pragma unroll 1
-            for (int rr = warp; rr < nrow; rr += 4) {
+            for (int rr = r0 + warp; rr < r1; rr += 4) {
                 const int rg = m0 + rr;
                 int32_t *o = p.topk_ids ? p.topk_ids + ((size_t)l * BNrows + rg) * p.K : nullptr;
-                const float *lrow = reinterpret_cast<const float *>(base) + (size_t)rr * (BN + 1);
+                const float *lrow = reinterpret_cast<const float *>(base) + (size_t)rr * LS;
                 const Bits<NE> wr = topk_warp_row<NE>(lrow, p.K, o, lane);
                 if (lane == 0) {
                     unsigned long long *dst = p.bits + ((size_t)(ridx[rr] / p.N) * p.L + l) * EW;
@@ -564,7 +574,7 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
         }
         }
     }
-    if (S > 1) cluster_sync();                // partials stay alive until the leader has read them
+    if (S > 1) cluster_sync();                // partials stay alive until every split has read them
 }
 
 __global__ void k_finalize(int B, int L, int EW, const unsigned long long *bits, int32_t *count, int32_t *total)
@@ -703,7 +713,7 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     static int max_clusters[2][5] = {{-1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1}};
     const int wide = E == 256;   // 256 experts: N = 256 MMA, 48 KB stages, 4-stage ring, 1 CTA/SM
     static std::mutex mc_mu;
-    while (S > 1) {
+    while (S > 1 && !wide) {   // 256 experts: 1 CTA/SM and ≤ 4-CTA clusters — placed without the query
         int mc;
         {
             std::lock_guard<std::mutex> g(mc_mu);

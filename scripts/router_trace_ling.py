@@ -8,7 +8,7 @@ P, Q, n = gen.trees(3, B, N, 6, 10)
 sel = ev.evict_select(cu(P), cu(Q), cu(gen.cost_table(N)), n_nodes=cu(n))
 b = ev.evict_build_verify_tree(cu(P), sel["keep_bits"], n_nodes=cu(n))
 h = gen.hidden_cuda(11, B, N, L, d, mode=1); w = gen.wgate_cuda(12, L, E, d, mode=1, scale_log2=-5)
-tr = ev._Trees(B, N, None, None, None); rt = ev._Router(L, E, K, d, ev._p(h), ev._p(w), 0)
+tr = ev._Trees(B, N, None, None, None); T_rows = int(b["verify_offsets"][-1]); rt = ev._Router(L, E, K, d, ev._p(h), ev._p(w), T_rows)
 uc = torch.empty((B, L), dtype=torch.int32, device="cuda"); ut = torch.empty(B, dtype=torch.int32, device="cuda")
 ub = torch.empty((B, L, 4), dtype=torch.int64, device="cuda")
 trace = torch.zeros(256, dtype=torch.int64, device="cuda")
@@ -23,3 +23,4 @@ print("mma full-wait passed (us):", [round((x - t0) / 1e3, 2) for x in t[0:32]])
 print("tma issue (us):", [round((x - t0) / 1e3, 2) for x in t[64:96]])
 print("producer stage start (us):", [round((x - t0) / 1e3, 2) for x in t[128:160]])
 print("epi start/tfull/end/sync/staged/topk/prepass/scan:", [round((x - t0) / 1e3, 2) for x in t[192:200]], "inserts", t[200], "scan cycles", t[201])
+print("splits", int(t[251]))
