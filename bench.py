@@ -257,9 +257,24 @@ def cpu_baseline(args, k_star_mean):
     oracle.build_verify_tree(P, o["keep_bits"], n_nodes=n)
     oracle.expert_union(o["keep_bits"], ids, N_EXPERTS, n_nodes=n, threads=threads)
     dt = time.perf_counter() - t0
+    # one-thread rate on the first 20,000 of the same trees (both are reported)
+    S1 = min(S, 20_000)
+    t0 = time.perf_counter()
+    o1 = oracle.select(P[:S1], Q[:S1], cost, n_nodes=n[:S1], threads=1)
+    oracle.build_verify_tree(P[:S1], o1["keep_bits"], n_nodes=n[:S1])
+    oracle.expert_union(o1["keep_bits"], ids[:S1], N_EXPERTS, n_nodes=n[:S1], threads=1)
+    dt1 = time.perf_counter() - t0
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+    except OSError:
+        pass
     return {"value": S / dt, "unit": "trees/s", "cores": threads, "kind": "oracle",
+            "one_thread_value": S1 / dt1, "cpu_model": model,
             "sample": f"first {S} trees of rank 0's c5 shard (seed {SEED}); oracle select+build+"
-                      f"union (C, fp64 sums) on {threads} host threads; generation excluded"}
+                      f"union (C, fp64 sums) on {threads} host threads (one_thread_value: first {S1} "
+                      f"on 1 thread); generation excluded"}
 
 
 def latency_b64(ev, torch, gen, N=60, steps=6, topk=10, seed=4, replays=2000):
