@@ -87,3 +87,39 @@ def test_stats_match_host_sums(sweep):
     assert s[0] == M and s[4] == 0 and s[1] == k.sum() and s[3] == uc.sum()
     assert (s[6 + N:] == uc.sum(0)).all()
     assert (s[5:6 + N] == np.bincount(k, minlength=N + 1)).all()
+
+
+def test_all_trees_match_oracle(sweep):
+    """Every one of the 1,000,000 trees (parity over the whole C5 set): k*,
+    keep bits, e_hat / utility and the per-layer union counts against the oracle run on the
+    host copies of the same inputs (all host threads)."""
+    import os
+    P = sweep["P"].cpu().numpy()
+    Q = sweep["Q"].cpu().numpy()
+    n = sweep["n"].cpu().numpy()
+    ids = sweep["ids"].cpu().numpy()
+    out = sweep["out"]
+    threads = os.cpu_count() or 8
+    o = oracle.select(P, Q, gen.cost_table(N), n_nodes=n, threads=threads)
+    kg = out["k_star"].cpu().numpy()
+    keep_g = out["keep_bits"].cpu().numpy().view(np.uint64)
+    diff = np.flatnonzero((kg != o["k_star"]) | (keep_g != o["keep_bits"]).any(axis=1) |
+                          (out["status"].cpu().numpy().astype(np.uint32) != o["status"]))
+    # the only admissible differences are reported ties (rule 3 of oracle/parity.py)
+    if diff.size:
+        sub = {k: v[diff] for k, v in o.items()}
+        gsub = {k: out[k].cpu().numpy()[diff] for k in ("k_star", "e_hat", "utility", "keep_bits", "status")}
+        res, msgs = compare_select(sub, gsub, n_nodes=n[diff])
+        assert not msgs, msgs[:3]
+        assert res["mismatch"] == 0
+    same = (o["status"] == 0)
+    same[diff] = False                                    # ties were checked above at the GPU's k*
+    for key in ("e_hat", "utility"):
+        ref = o[key][same]
+        got = out[key].cpu().numpy()[same].astype(np.float64)
+        assert np.all(np.abs(got - ref) <= 1e-5 * np.abs(ref)), key
+    keep = downstream_keep(o, {"k_star": kg})
+    ou = oracle.expert_union(keep, ids, E, n_nodes=n, threads=threads)
+    assert (ou["union_count"] == out["union_count"].cpu().numpy()).all()
+    assert (ou["union_total"] == out["union_total"].cpu().numpy()).all()
+    assert (ou["union_bits"] == out["union_bits"].cpu().numpy().view(np.uint64).reshape(ou["union_bits"].shape)).all()
