@@ -205,3 +205,43 @@ def test_parity_cluster_sizes(B, greedy):
     o = ov.verify_sample(P, kb, tok, probs, ua, ub, mode=mode, n_nodes=n, verify_offsets=off)
     g = _gpu(P, n, kb, tok, probs, ua, ub, V, greedy)
     _compare(o, g)
+
+
+@pytest.mark.parametrize("greedy", [False, True])
+def test_bench_configuration_sampled(greedy):
+    """bench.py's verify workload: 1024 trees (16 copies of a 64-tree batch, each copy with its own
+    uniforms) at V = 151936 — the 1-CTA-per-tree launch the bench times — with 64 sampled trees
+    checked one by one against the oracle."""
+    import torch
+    import oracle
+    import paper_2605_00342_b200 as ev
+    V, B0, N, rep = gv.QWEN3_VOCAB, 64, 60, 16
+    P, Q, n = gen.trees(21, B0, N, 6, 10)
+    keep = oracle.select(P, Q, gen.cost_table(N), n_nodes=n)["keep_bits"]
+    ob = oracle.build_verify_tree(P, keep, n_nodes=n)
+    off = ob["verify_offsets"]
+    T0 = int(off[-1])
+    tok = gv.draft_tokens(21, P, V, n_nodes=n)
+    rows = gv.target_rows(21, P, Q, tok, np.repeat(np.arange(B0), np.diff(off)), ob["kept_index"][:T0], V, n_nodes=n)
+    ua, ub = gv.uniforms(21, B0 * rep, N)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    offs = np.concatenate([off[:-1] + r * T0 for r in range(rep)] + [[rep * T0]]).astype(np.int32)
+    tile = lambda a: np.concatenate([a[:T0]] * rep)  # noqa: E731
+    ri = np.concatenate([ob["retrieve_index"][:T0] + r * B0 * N for r in range(rep)]).astype(np.int32)
+    probs = cu(rows).repeat(rep, 1)
+    g = ev.evict_verify_sample(cu(offs), cu(tile(ob["next_token"])), cu(tile(ob["next_sibling"])), cu(ri),
+                               cu(np.tile(tok, (rep, 1))), probs, u_accept=cu(ua.view(np.int32)),
+                               u_bonus=cu(ub.view(np.int32)), greedy=greedy)
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in g.items()}
+    mode = ov.GREEDY if greedy else ov.SAMPLE
+    sample = np.random.default_rng(3).choice(B0 * rep, 64, replace=False)
+    for bb in sample:
+        b = int(bb) % B0
+        kept = [i for i in range(int(n[b])) if (int(keep[b, 0]) >> i) & 1]
+        row_of_slot = [int(off[b]) + s for s in range(len(kept))]
+        st, path, bonus = ov.verify_one(P[b].tolist(), int(n[b]), kept, tok[b].tolist(), row_of_slot, rows, mode,
+                                        ua[bb].tolist(), int(ub[bb]))
+        assert st == 0 and int(g["status"][bb]) == 0
+        assert int(g["accept_len"][bb]) == len(path) and g["accepted_slots"][bb, :len(path)].tolist() == path, bb
+        assert int(g["bonus_token"][bb]) == bonus, bb
