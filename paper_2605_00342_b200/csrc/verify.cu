@@ -208,15 +208,17 @@ __device__ int row_argmax(const float *row, int V, Smem &s, int tid, int par)
     bool bad = false;
     const int V4 = V >> 2;
     const float4 *r4 = reinterpret_cast<const float4 *>(row);
-    // four float4 loads per thread in flight per iteration
+    // float4 loads per thread in flight per iteration: 8 for a whole-CTA row (throughput batches),
+    // 4 when a cluster shares the row (small batches, where the deeper unroll cost latency)
     constexpr int kStep = CL * kThreads;
-    for (int i0 = tid + (int)r * kThreads; i0 < V4; i0 += 4 * kStep) {
-        float4 x[4];
+    constexpr int DEPTH = CL == 1 ? 8 : 4;
+    for (int i0 = tid + (int)r * kThreads; i0 < V4; i0 += DEPTH * kStep) {
+        float4 x[DEPTH];
 #pragma unroll
-        for (int h = 0; h < 4; h++)
+        for (int h = 0; h < DEPTH; h++)
             x[h] = i0 + h * kStep < V4 ? __ldcs(r4 + i0 + h * kStep) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int h = 0; h < 4; h++) {
+        for (int h = 0; h < DEPTH; h++) {
             const int i = i0 + h * kStep;
             const uint32_t u[4] = {__float_as_uint(x[h].x), __float_as_uint(x[h].y), __float_as_uint(x[h].z),
                                    __float_as_uint(x[h].w)};
