@@ -256,8 +256,11 @@ evict_status_t evict_select_build_union_policy(const evict_trees_t *trees, const
  *            launch only (grid, k-split, ring depth).  Contract: T ≤
  *            max_rows (T is device-resident, so the host cannot check it;
  *            rows at or past ceil(max_rows/128)·128 would not be routed).
- * Supported: E ∈ {128, 256} (256: Ling-flash-2.0; N = 256 MMA,
- *   union_bits [B][L][4]), d % 64 == 0, K ≤ 16, L·B·N < 2^31.
+ * Supported: 1 ≤ E ≤ 256 (E ≤ 128: N = 128 MMA; 128 < E ≤ 256, e.g.
+ *   Ling-flash-2.0: N = 256 MMA; the expert rows past E are
+ *   zero-filled by TMA and their logits masked to -inf before the TopK),
+ *   union_bits [B][L][ceil(E/64)], d % 64 == 0, K ≤ min(16, E), L·B·N < 2^31;
+ *   E > 256 → EVICT_ERR_UNSUPPORTED.
  * ------------------------------------------------------------------------- */
 typedef struct {
     int32_t num_layers;
@@ -313,7 +316,10 @@ evict_status_t evict_union_curve(const evict_trees_t *trees, const int32_t *orde
  *   cost[k-1] = c0 + c_union·Ū(k) + c_tok·k, fp64 arithmetic, stored fp32;
  *   +inf when no tree has k nodes (an infeasible k, reading Z10).
  * status may be NULL.  workspace: evict_profile_workspace_bytes(N) bytes,
- * 8-byte aligned, overwritten.  The result is a valid evict_select cost table.
+ * 8-byte aligned, overwritten.  Requires c0 > 0, c_union ≥ 0, c_tok ≥ 0 and
+ * c0 + 256·c_union + N·c_tok < 3e38 (else EVICT_ERR_INVALID_ARG), so the
+ * result is always a valid evict_select cost table (entries ≥ c0, finite
+ * or +inf for an infeasible k).
  * ------------------------------------------------------------------------- */
 size_t evict_profile_workspace_bytes(int32_t max_nodes);
 evict_status_t evict_profile_cost(int32_t batch, int32_t max_nodes, int32_t num_layers,

@@ -275,7 +275,7 @@ extern "C" evict_status_t evict_union_curve(const evict_trees_t *trees, const in
         return EVICT_ERR_INVALID_ARG;
     }
     if ((uintptr_t)rt->ids & 15) return EVICT_ERR_INVALID_ARG;
-    if (evict::dev_sms() <= 0) return EVICT_ERR_UNSUPPORTED;
+    if (!evict::dev_supported()) return EVICT_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     const int blocks = (trees->batch + kWarpsC - 1) / kWarpsC;
     const int R = (rt->num_layers + 31) / 32;
@@ -309,8 +309,13 @@ extern "C" evict_status_t evict_profile_cost(int32_t batch, int32_t max_nodes, i
         ((uintptr_t)workspace & 7))
         return EVICT_ERR_INVALID_ARG;
     if (!isfinite(c0) || !isfinite(c_union) || !isfinite(c_tok)) return EVICT_ERR_INVALID_ARG;
+    // every entry must be a valid evict_select cost: C(k) ≥ c0 > 0 and finite in fp32
+    // (Ū(k) ≤ E ≤ EVICT_MAX_EXPERTS, k ≤ N)
+    if (!(c0 > 0.f) || c_union < 0.f || c_tok < 0.f) return EVICT_ERR_INVALID_ARG;
+    if ((double)c0 + (double)c_union * EVICT_MAX_EXPERTS + (double)c_tok * max_nodes > 3.0e38)
+        return EVICT_ERR_INVALID_ARG;
     const int sms = evict::dev_sms();
-    if (sms <= 0) return EVICT_ERR_UNSUPPORTED;
+    if (sms <= 0 || !evict::dev_supported()) return EVICT_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long *sums = reinterpret_cast<unsigned long long *>(workspace);
     unsigned long long *cnts = sums + max_nodes;

@@ -63,7 +63,7 @@ extern "C" evict_status_t evict_dispatch_create(int32_t n_bodies, const int32_t 
         if (!body_graphs[i] || lengths[i] < 0 || (i && lengths[i] <= lengths[i - 1])) return EVICT_ERR_INVALID_ARG;
         lens.v[i] = lengths[i];
     }
-    if (evict::dev_sms() <= 0) return EVICT_ERR_UNSUPPORTED;
+    if (!evict::dev_supported()) return EVICT_ERR_UNSUPPORTED;
     evict_dispatch_s *d = new (std::nothrow) evict_dispatch_s();
     if (!d) return EVICT_ERR_CUDA;
     auto fail = [&](void) {

@@ -389,7 +389,7 @@ extern "C" evict_status_t evict_build_draft_tree(int32_t batch, int32_t steps, i
         return EVICT_ERR_INVALID_ARG;
     if ((long long)1 + topk + (long long)(steps - 1) * topk * topk > EVICT_DRAFT_MAX_POOL) return EVICT_ERR_INVALID_ARG;
     if (!child_tokens || !child_probs || !parent || !q || !tokens || !n_nodes) return EVICT_ERR_INVALID_ARG;
-    if (evict::dev_sms() <= 0) return EVICT_ERR_UNSUPPORTED;
+    if (!evict::dev_supported()) return EVICT_ERR_UNSUPPORTED;
     using namespace evict::draft;
     const int P = 1 + topk + (steps - 1) * topk * topk;
     const int lmax = (topk * topk < max_nodes - 1 ? topk * topk : max_nodes - 1) > 0

@@ -62,6 +62,7 @@ bool wide(int N) { return N > 64; }  // 4 nodes per lane, else 2
 }  // namespace
 
 int dev_sms() { return dev_info().sms; }
+bool dev_supported() { return dev_info().ok != 0; }
 
 }  // namespace evict
 

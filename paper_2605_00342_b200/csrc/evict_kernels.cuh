@@ -424,6 +424,30 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
         if (lane == 0) st_release(states + tile, (tile == 0 ? kInc : kAgg) | (uint64_t)agg);
         int next = 0;
         if (lane == 0) next = (int)atomicAdd(ticket, 1u);
+        // ---------------- look-back for the tile prefix, right after the publish: predecessors
+        // publish their inclusive prefix just as early, so the walk ends within ~1 round (run
+        // after the union, it walked back over every warp still in its union: ~300 instructions
+        // per tree of polling at 24 warps/SM)
+        unsigned prefix = 0;
+        if (tile > 0) {
+            int end = tile;
+            while (true) {
+                const int j = end - 1 - lane;
+                const uint64_t sv = j >= 0 ? ld_acquire(states + j) : kInc;
+                const unsigned flag = (unsigned)(sv >> 62);
+                const unsigned inc_mask = __ballot_sync(kFull, flag == 2);
+                const unsigned zero_mask = __ballot_sync(kFull, flag == 0);
+                const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
+                const unsigned before = first_inc == 32 ? kFull : ((1u << first_inc) - 1u);
+                if (zero_mask & before) continue;
+                const unsigned v = lane <= first_inc ? (unsigned)(sv & kValMask) : 0u;
+                prefix += __reduce_add_sync(kFull, v);
+                if (first_inc < 32) break;
+                end -= 32;
+            }
+            if (lane == 0) st_release(states + tile, kInc | (uint64_t)(prefix + (unsigned)agg));
+        }
+        off_local += (int)prefix;
         // ---------------- A2: expert union, one warp per tree
         if (do_union) {
             if constexpr (FLAGS) {
@@ -459,27 +483,6 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 __syncwarp();
             }
         }
-        // ---------------- look-back for the tile prefix
-        unsigned prefix = 0;
-        if (tile > 0) {
-            int end = tile;
-            while (true) {
-                const int j = end - 1 - lane;
-                const uint64_t sv = j >= 0 ? ld_acquire(states + j) : kInc;
-                const unsigned flag = (unsigned)(sv >> 62);
-                const unsigned inc_mask = __ballot_sync(kFull, flag == 2);
-                const unsigned zero_mask = __ballot_sync(kFull, flag == 0);
-                const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
-                const unsigned before = first_inc == 32 ? kFull : ((1u << first_inc) - 1u);
-                if (zero_mask & before) continue;
-                const unsigned v = lane <= first_inc ? (unsigned)(sv & kValMask) : 0u;
-                prefix += __reduce_add_sync(kFull, v);
-                if (first_inc < 32) break;
-                end -= 32;
-            }
-            if (lane == 0) st_release(states + tile, kInc | (uint64_t)(prefix + (unsigned)agg));
-        }
-        off_local += (int)prefix;
         next = __shfl_sync(kFull, next, 0);
         // ---------------- C: verify-tree emit, sub-warp per tree
 #pragma unroll 1

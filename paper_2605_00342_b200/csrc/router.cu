@@ -35,6 +35,7 @@ template <int NE> __host__ __device__ constexpr int stage_bytes() { return A_BYT
 constexpr int THREADS = 192;
 constexpr int NPROD = 128;
 constexpr int KMAX = 16;
+constexpr int kMaxDev = 64;        // per-device host caches (function attributes, cluster occupancy)
 template <int NE>
 __host__ __device__ constexpr int smem_bytes(int stages)
 {
@@ -91,6 +92,16 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y)
+        : "memory");
+}
+
+// W_g k-block as a 3D box {64 cols, NE experts, 1 layer} of the [L][E][d] tensor: expert rows
+// ≥ E (E < NE) fall outside the tensor and are zero-filled by TMA (their logits are masked).
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int x, int y, int z)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(x), "r"(y), "r"(z)
         : "memory");
 }
 
@@ -337,8 +348,10 @@ struct Params {
     const int32_t *verify_offsets; // [B+1]
     const int32_t *retrieve_index; // [cap]
     int L, B, N, d, K;
+    int E;                         // real experts (≤ NE): logits of columns ≥ E are masked to -inf
+    int EWo;                       // output bit words per (tree, layer) = ceil(E/64)
     int splits;                    // k-splits = cluster size along z (1: no cluster)
-    unsigned long long *bits;      // [B][L][NE/64]
+    unsigned long long *bits;      // [B][L][EWo]
     int32_t *topk_ids;             // [L][B*N][K] or null
     float *dbg_logits;             // [L][B*N][128] or null (debug entry point only)
     long long *trace;              // [256] globaltimer trace of CTA (0,0) or null (debug only)
@@ -440,6 +453,10 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
         for (int chunk = 0; chunk < BN / 32; chunk++) {
             float v[32];
             tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + chunk * 32, v);
+            if (chunk * 32 + 32 > p.E) {   // E < NE: padding experts never enter the TopK
+#pragma unroll
+                for (int j = 0; j < 32; j++) v[j] = chunk * 32 + j < p.E ? v[j] : -__int_as_float(0x7f800000);
+            }
             float4 *l4 = reinterpret_cast<float4 *>(lg + chunk * 32);
 #pragma unroll
             for (int q = 0; q < 8; q++) l4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -473,7 +490,7 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
                 if (i >= STAGES) mbar_wait(empty0 + 8 * s, ((i / STAGES) - 1) & 1);
                 if (tr0 && i < 64) p.trace[64 + i] = gtimer();
                 mbar_arrive_tx(full0 + 8 * s, B_BYTES + 512u * ng);
-                tma_load_2d(Bs(s), &wmap, full0 + 8 * s, kb * BK, l * BN);
+                tma_load_3d(Bs(s), &wmap, full0 + 8 * s, kb * BK, 0, l);
                 for (int g4 = 0; g4 < ng; g4++) {
                     int rr[4];
 #pragma unroll
@@ -541,10 +558,10 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
                 const float *lrow = reinterpret_cast<const float *>(base) + (size_t)rr * LS;
                 const Bits<NE> wr = topk_warp_row<NE>(lrow, p.K, o, lane);
                 if (lane == 0) {
-                    unsigned long long *dst = p.bits + ((size_t)(ridx[rr] / p.N) * p.L + l) * EW;
+                    unsigned long long *dst = p.bits + ((size_t)(ridx[rr] / p.N) * p.L + l) * p.EWo;
 #pragma unroll
                     for (int h = 0; h < EW; h++)
-                        atomicOr(dst + h, (unsigned long long)wr.w[2 * h] | ((unsigned long long)wr.w[2 * h + 1] << 32));
+                        if (h < p.EWo) atomicOr(dst + h, (unsigned long long)wr.w[2 * h] | ((unsigned long long)wr.w[2 * h + 1] << 32));
                 }
             }
             if (tr0 && threadIdx.x == 0) p.trace[197] = gtimer();
@@ -565,10 +582,10 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
 #pragma unroll
             for (int q = 0; q < NE / 32; q++) o[q] = __reduce_or_sync(0xffffffffu, in ? wq.w[q] : 0u);
             if (lane == leader) {
-                unsigned long long *dst = p.bits + ((size_t)tb * p.L + l) * EW;
+                unsigned long long *dst = p.bits + ((size_t)tb * p.L + l) * p.EWo;
 #pragma unroll
                 for (int h = 0; h < EW; h++)
-                    atomicOr(dst + h, (unsigned long long)o[2 * h] | ((unsigned long long)o[2 * h + 1] << 32));
+                    if (h < p.EWo) atomicOr(dst + h, (unsigned long long)o[2 * h] | ((unsigned long long)o[2 * h + 1] << 32));
             }
             pending &= ~grp;
         }
@@ -655,18 +672,21 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     if (rt->top_k < 1 || rt->top_k > EVICT_MAX_TOPK || rt->top_k > rt->num_experts) return EVICT_ERR_INVALID_ARG;
     if (rt->hidden_dim < 64 || rt->hidden_dim % 64) return EVICT_ERR_INVALID_ARG;
     if (((uintptr_t)rt->hidden | (uintptr_t)rt->w_gate) & 15) return EVICT_ERR_INVALID_ARG;
-    if (rt->num_experts != 128 && rt->num_experts != 256) return EVICT_ERR_UNSUPPORTED;
-    if (evict::dev_sms() <= 0) return EVICT_ERR_UNSUPPORTED;
+    if (rt->num_experts < 1 || rt->num_experts > 256) return EVICT_ERR_UNSUPPORTED;
+    if (!evict::dev_supported()) return EVICT_ERR_UNSUPPORTED;
     EncodeTiledFn enc = encode_fn();
     if (!enc) return EVICT_ERR_UNSUPPORTED;
     const int L = rt->num_layers, E = rt->num_experts, d = rt->hidden_dim;
     const int B = trees->batch, N = trees->max_nodes;
+    // the MMA width: N = 128 for E ≤ 128, N = 256 for 128 < E ≤ 256 (columns ≥ E masked)
+    const int wide = E > 128;
+    const int NE = wide ? 256 : 128;
     CUtensorMap map;
-    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)L * E};
-    cuuint64_t strides[1] = {(cuuint64_t)d * 2};
-    cuuint32_t box[2] = {BK, (cuuint32_t)E};   // one W_g k-block: all E experts (≤ 256 rows)
-    cuuint32_t estr[2] = {1, 1};
-    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(rt->w_gate), dims, strides, box, estr,
+    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)E, (cuuint64_t)L};
+    cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)E * d * 2};
+    cuuint32_t box[3] = {BK, (cuuint32_t)NE, 1};   // one W_g k-block: NE expert rows, zero-filled past E
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(rt->w_gate), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return EVICT_ERR_INVALID_ARG;
@@ -680,19 +700,23 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return EVICT_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
-    static std::once_flag attr_once;
-    std::call_once(attr_once, [] {
+    // function attributes are per device: opt in to > 48 KB of shared memory once per device
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return EVICT_ERR_UNSUPPORTED;
+    static std::once_flag attr_once[kMaxDev];
+    std::call_once(attr_once[dev], [] {
         cudaFuncSetAttribute(k_router<128, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>(6));
         cudaFuncSetAttribute(k_router<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<128>(3));
         cudaFuncSetAttribute(k_router<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<256>(4));
     });
-    const int EW = E / 64;
+    const int EW = (E + 63) / 64;   // output words per (tree, layer)
     if (cudaMemsetAsync(union_bits, 0, sizeof(uint64_t) * (size_t)B * L * EW, s) != cudaSuccess) return EVICT_ERR_CUDA;
     Params p;
     p.hidden = (const uint16_t *)rt->hidden;
     p.verify_offsets = verify_offsets;
     p.retrieve_index = retrieve_index;
     p.L = L; p.B = B; p.N = N; p.d = d; p.K = rt->top_k;
+    p.E = E; p.EWo = EW;
     p.bits = reinterpret_cast<unsigned long long *>(union_bits);
     p.topk_ids = topk_ids;
     p.dbg_logits = dbg_logits;
@@ -710,14 +734,15 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
     if (S > KB) S = KB;
     // clusters are placed GPC by GPC: take the largest S whose tiles·L clusters are all
     // co-resident (a second wave would double the time)
-    static int max_clusters[2][5] = {{-1, -1, -1, -1, -1}, {-1, -1, -1, -1, -1}};
-    const int wide = E == 256;   // 256 experts: N = 256 MMA, 48 KB stages, 4-stage ring, 1 CTA/SM
+    // (per device: the query answers for the current device)
+    static int max_clusters[kMaxDev][5] = {};
+    static bool mc_known[kMaxDev][5] = {};
     static std::mutex mc_mu;
     while (S > 1 && !wide) {   // 256 experts: 1 CTA/SM and ≤ 4-CTA clusters — placed without the query
         int mc;
         {
             std::lock_guard<std::mutex> g(mc_mu);
-            if (max_clusters[wide][S] < 0) {
+            if (!mc_known[dev][S]) {
                 cudaLaunchConfig_t q = {};
                 q.gridDim = dim3((unsigned)S, 1u, 1u);
                 q.blockDim = dim3(THREADS, 1, 1);
@@ -732,9 +757,10 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
                 int n = 0;
                 const cudaError_t qe = wide ? cudaOccupancyMaxActiveClusters(&n, k_router<256, 4>, &q)
                                             : cudaOccupancyMaxActiveClusters(&n, k_router<128, 6>, &q);
-                max_clusters[wide][S] = qe == cudaSuccess ? n : 0;
+                max_clusters[dev][S] = qe == cudaSuccess ? n : 0;
+                mc_known[dev][S] = true;
             }
-            mc = max_clusters[wide][S];
+            mc = max_clusters[dev][S];
         }
         if (mc >= tiles * L) break;
         S--;

@@ -122,7 +122,7 @@ extern "C" evict_status_t evict_batch_stats(int32_t batch, int32_t max_nodes, in
     if (!k_star || !e_hat || !utility || !stats || !dstats || (num_layers > 0 && !union_count))
         return EVICT_ERR_INVALID_ARG;
     const int sms = evict::dev_sms();
-    if (sms <= 0) return EVICT_ERR_UNSUPPORTED;
+    if (sms <= 0 || !evict::dev_supported()) return EVICT_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     const int len = 6 + max_nodes + num_layers;
     if (cudaMemsetAsync(stats, 0, sizeof(int64_t) * len, s) != cudaSuccess) return EVICT_ERR_CUDA;

@@ -194,6 +194,8 @@ struct Smem {
     U3 pre;             // exclusive prefix before the crossing chunk
     int32_t k, plen, node, nrej, cross, bonus;
     uint32_t st;
+    uint32_t rbad;      // bonus row: invalid entries found by any CTA of the cluster (CTA 0's copy),
+                        // merged into st by CTA 0 after the cluster barrier (peers never write st)
 };
 
 // Cluster-wide argmax over one row: (value desc, index asc); CTA r of CL scans float4 slots
@@ -463,11 +465,16 @@ __device__ void bonus_fast(const float *row, int V, uint32_t ub, Smem &s, int ti
         }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) {
-        if constexpr (CL == 1) atomicOr(&s.st, EVICT_TREE_BAD_PROB);
-        else cl_or_u32(cl_map(&s.st, 0), EVICT_TREE_BAD_PROB);
+        if constexpr (CL == 1) atomicOr(&s.rbad, EVICT_TREE_BAD_PROB);
+        else cl_or_u32(cl_map(&s.rbad, 0), EVICT_TREE_BAD_PROB);
     }
     if constexpr (CL > 1) cl_sync(); else __syncthreads();
-    if (r != 0 || s.st) return;                     // the rest runs in CTA 0
+    if (r != 0) return;                             // the rest runs in CTA 0
+    // s.st was 0 on entry (uniform across the cluster); bad bonus-row entries arrive in rbad
+    if (s.rbad) {
+        if (tid == 0) s.st |= s.rbad;
+        return;
+    }
     const int nrej = s.nrej;
     if (tid == 0) {
         double r = 0.0;
@@ -589,6 +596,7 @@ __global__ void __launch_bounds__(kThreads) k_verify(evict_verify_batch_t vb, co
         s.st = k > N ? EVICT_TREE_BAD_SIZE : k < 1 ? EVICT_TREE_BAD_KEEP : 0u;   // k = 0: empty keep set
         s.k = k;
         s.nrej = 0;
+        s.rbad = 0u;
     }
     if (tid < 16) (&s.cbad[0][0])[tid] = 0u;
     if constexpr (CL > 1) cl_sync(); else __syncthreads();   // every CTA of the cluster is live
@@ -613,12 +621,14 @@ __global__ void __launch_bounds__(kThreads) k_verify(evict_verify_batch_t vb, co
         }
     }
     __syncthreads();
-    if (!s.st) {
+    // parent slots and the orphan check run unless size/keep already failed (a bad token alone
+    // must not hide a BAD_KEEP: the first failing check in header order is reported)
+    if (!(s.st & (EVICT_TREE_BAD_SIZE | EVICT_TREE_BAD_KEEP))) {
         for (int q = tid; q < k; q += kThreads)
             for (int c = s.nt[q]; c != -1; c = s.ns[c]) s.ps[c] = q;
     }
     __syncthreads();
-    if (!s.st) {
+    if (!(s.st & (EVICT_TREE_BAD_SIZE | EVICT_TREE_BAD_KEEP))) {
         for (int q = 1 + tid; q < k; q += kThreads)
             if (s.ps[q] < 0) atomicOr(&s.st, EVICT_TREE_BAD_KEEP);   // an orphan slot
     }
@@ -742,7 +752,7 @@ extern "C" evict_status_t evict_verify_sample(const evict_verify_batch_t *vb, co
     if (mode & ~(1 | EVICT_VERIFY_EXACT)) return EVICT_ERR_INVALID_ARG;
     if ((mode & 1) == EVICT_VERIFY_SAMPLE && (!u_accept || !u_bonus)) return EVICT_ERR_INVALID_ARG;
     const int sms = evict::dev_sms();
-    if (sms <= 0) return EVICT_ERR_UNSUPPORTED;
+    if (sms <= 0 || !evict::dev_supported()) return EVICT_ERR_UNSUPPORTED;
     // cluster size: split each tree's row over CL CTAs only until one wave of the 4 resident
     // CTAs per SM is full (64 trees → 8, 300 → 2, ≥ 592 → 1).  Past that a cluster only adds
     // redundant prologues and barriers: at 1024 trees CL = 1 / 2 / 4 / 8 measured 75% / 69% /

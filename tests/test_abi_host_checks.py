@@ -83,3 +83,48 @@ def test_dispatch_checks(lib):
     lib.evict_dispatch_destroy(None)                           # a no-op on NULL
     assert lib.evict_dispatch_create(3, lens, bodies, None, p(FAKE), None, ctypes.byref(out)) == UNSUPPORTED
     assert not out.value
+
+
+def _profile(lib, c0=10.47, cu=0.0915, ct=0.15, N=60):
+    p = ctypes.c_void_p
+    ws = lib.evict_profile_workspace_bytes(N)
+    return lib.evict_profile_cost(8, N, 48, None, p(FAKE), None, c0, cu, ct, p(FAKE), p(FAKE), ws, None)
+
+
+def test_profile_cost_checks(lib):
+    """Coefficients that could give cost[k] <= 0 or overflow fp32 are rejected on the host (the
+    result must always be a valid evict_select cost table)."""
+    assert _profile(lib, c0=0.0) == INVALID
+    assert _profile(lib, c0=-1.0) == INVALID
+    assert _profile(lib, cu=-0.5) == INVALID
+    assert _profile(lib, ct=-0.1) == INVALID
+    assert _profile(lib, c0=float("nan")) == INVALID
+    assert _profile(lib, cu=3.0e38) == INVALID                # 256 * c_union overflows fp32
+    assert _profile(lib, c0=1e-30, cu=0.0, ct=0.0) == UNSUPPORTED   # valid, no sm_100 device here
+    assert _profile(lib) == UNSUPPORTED
+
+
+def test_router_checks(lib):
+    """evict_router_union: E > 256 is UNSUPPORTED, a well-formed E < 128 call (the C1 toy shape)
+    reaches the device check (no sm_100 device here)."""
+    p = ctypes.c_void_p
+
+    class Trees(ctypes.Structure):
+        _fields_ = [("batch", ctypes.c_int32), ("max_nodes", ctypes.c_int32), ("n_nodes", p),
+                    ("parent", p), ("q", p)]
+
+    class Router(ctypes.Structure):
+        _fields_ = [("num_layers", ctypes.c_int32), ("num_experts", ctypes.c_int32), ("top_k", ctypes.c_int32),
+                    ("hidden_dim", ctypes.c_int32), ("hidden", p), ("w_gate", p), ("max_rows", ctypes.c_int32)]
+
+    tr = Trees(1, 8, None, None, None)
+
+    def call(E, K=2, d=64):
+        rt = Router(2, E, K, d, FAKE, FAKE, 0)
+        return lib.evict_router_union(ctypes.byref(tr), p(FAKE), p(FAKE), ctypes.byref(rt), p(FAKE), None,
+                                      p(FAKE), None, None)
+
+    assert call(320) == UNSUPPORTED
+    assert call(8, K=9) == INVALID                            # K > E
+    assert call(8, d=96) == INVALID                           # d % 64
+    assert call(8) == UNSUPPORTED                             # C1 toy shape: supported, no device here

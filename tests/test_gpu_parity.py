@@ -271,11 +271,21 @@ def test_union_bad_expert_and_hist(ev):
 
 
 # ------------------------------------------------------------------ fused
+def _cfg(name):
+    """BASELINE configs, plus c2 trees with 56 layers: L·2 = 112 id slots runs the R = 4 register
+    rounds of k_fused (L ≤ 48: R = 3; C3's 94 layers: R = 8, two flag passes)."""
+    if name == "c2_l56":
+        return dict(gen.CONFIGS["c2"], L=56)
+    return gen.CONFIGS[name]
+
+
 @pytest.mark.parametrize("with_order", [True, False])
 @pytest.mark.parametrize("name,fmt", [("c2", "u8"), ("c4", "u8"), ("c4_60", "i32"),
-                                      ("c4_60", "mask"), ("paper", "u8"), ("ling", "u8"), ("ling", "mask")])
+                                      ("c4_60", "mask"), ("paper", "u8"), ("ling", "u8"), ("ling", "mask"),
+                                      ("c3", "u8"), ("c3", "i32"), ("c3", "mask"), ("c2_l56", "u8"),
+                                      ("c2_l56", "i32"), ("c2_l56", "mask")])
 def test_fused_equals_oracle(ev, name, fmt, with_order):
-    c = gen.CONFIGS[name]
+    c = _cfg(name)
     B = 333
     N, L, E, K = c["N"], c["L"], c["E"], c["K"]
     P, Q, n = gen.trees(c["seed"] + 11, B, N, c["steps"], c["topk"])
@@ -418,11 +428,12 @@ def test_policy_rejects_bad_arguments(ev):
             ev.evict_select(P, Q, C, policy=bad)
 
 
-@pytest.mark.parametrize("name", ["c2", "ling"])
+@pytest.mark.parametrize("name", ["c2", "ling", "c3", "c2_l56"])
 def test_fused_lean_path(ev, name):
     """The serving configuration (u8 top-8 ids, no order row, no bit rows, no histogram) runs the
-    LEAN instantiation with marker-epoch flag blocks — E = 128 and the 256-expert layout."""
-    c = gen.CONFIGS[name]
+    LEAN instantiation with marker-epoch flag blocks — E = 128 and the 256-expert layout; C3's
+    94 layers (R = 8: two flag passes, no marker epochs) and 56 layers (R = 4)."""
+    c = _cfg(name)
     B = 777
     N, L, E, K = c["N"], c["L"], c["E"], c["K"]
     P, Q, n = gen.trees(c["seed"] + 3, B, N, c["steps"], c["topk"])

@@ -43,6 +43,11 @@ def kept_rows(ev, B, N, steps, topk, seed):
     (1, 60, 6, 10, 32, 4096, 8, 256),     # Ling-flash-2.0 shape (NEXT-4): 256 experts, batch 1
     (16, 60, 6, 10, 4, 4096, 8, 256),     # 256 experts, 16 trees
     (64, 128, 8, 10, 3, 2048, 16, 256),   # 256 experts, dense tiles, K = 16
+    (1, 8, 3, 2, 2, 64, 2, 8),            # c1 toy shape: 8 experts (N = 128 MMA, columns >= E masked)
+    (4, 60, 6, 10, 5, 512, 8, 64),        # 64 experts (one output word)
+    (7, 60, 6, 10, 3, 1024, 8, 100),      # E not a multiple of 64 (partial second word)
+    (16, 60, 6, 10, 3, 1024, 8, 200),     # 128 < E < 256: N = 256 MMA, masked tail
+    (64, 128, 8, 10, 2, 2048, 8, 96),     # dense tiles with a masked tail
 ])
 @pytest.mark.parametrize("hint", [False, True])
 def test_router_integer_inputs_bit_exact(ev, B, N, steps, topk, L, d, K, E, hint):
@@ -97,10 +102,60 @@ def test_router_vs_torch_normal_inputs(ev, E):
     assert checked > 0.7 * (checked + excluded)
 
 
+def test_router_c3_full_shape(ev):
+    """C3 at its real launch shape (Qwen3-235B-A22B: L = 94, d = 4096, E = 128,
+    top-8; B = 16 trees of 60 nodes): 1 tile x 94 layers runs unsplit on the 6-stage ring over
+    64 k-blocks.  Integer inputs: bit-exact against the fp64 oracle, with and without the
+    max_rows hint the bench passes."""
+    B, N, L, d, K, E = 16, 60, 94, 4096, 8, 128
+    P, n, keep, b = kept_rows(ev, B, N, 6, 10, seed=33)
+    h = gen.hidden(34, B, N, L, d, mode=0)
+    w = gen.wgate(35, L, E, d, mode=0)
+    o = oracle.router_union(keep, h, w, K, threads=8)
+    T = int(b["verify_offsets"][-1])
+    hb, wb = bf16(h), bf16(w)
+    for hint in (T, 0):
+        g = ev.evict_router_union(b["verify_offsets"], b["retrieve_index"], hb, wb, K, B, N, max_rows=hint)
+        assert not compare_union(o, {k: v.cpu().numpy() for k, v in g.items()}), hint
+
+
+def test_router_c1_toy_one_hot():
+    """C1: W_g rows e_0..e_7, hidden = 2 at the node's first expert and 1 at
+    its second, so TopK-2 reproduces the App. A routing table; the union counts along the
+    ranking must be the golden values ((3, 3) at k* = 3, total 6)."""
+    import json
+    import os
+    import torch
+    import paper_2605_00342_b200 as ev
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "toy_tree.json")))
+    L, E, K, d, N = 2, 8, 2, 64, 8
+    routing = np.stack([np.array(gold["routing_L0"]), np.array(gold["routing_L1"])], axis=0)
+    W = np.zeros((L, E, d), np.float32)
+    for l in range(L):
+        W[l, np.arange(E), np.arange(E)] = 1
+    H = np.zeros((L, N, d), np.float32)
+    for l in range(L):
+        for v in range(N):
+            H[l, v, routing[l, v, 0]] = 2
+            H[l, v, routing[l, v, 1]] = 1
+    tobf = lambda x: cu((x.view(np.uint32) >> 16).astype(np.uint16).view(np.int16)).view(torch.bfloat16)  # noqa: E731
+    P = np.array([gold["parent"]], np.int32)
+    for k in range(1, N + 1):
+        keep = np.zeros((1, 1), np.uint64)
+        for v in gold["order"][:k]:
+            keep[0, 0] |= np.uint64(1 << v)
+        b = ev.evict_build_verify_tree(cu(P), cu(keep.view(np.int64)))
+        g = ev.evict_router_union(b["verify_offsets"], b["retrieve_index"], tobf(H), tobf(W), K, 1, N)
+        assert g["union_count"][0].tolist() == gold["union_along_ranking"][k - 1], k
+        assert int(g["union_total"][0]) == gold["union_total_along_ranking"][k - 1]
+    # the Eq. 10 cut of the toy (k* = 3): (3, 3), total 6
+    assert gold["union_along_ranking"][2] == [3, 3] and gold["k_star"] == 3
+
+
 def test_router_rejects_unsupported(ev):
     import torch
     h = torch.zeros((1, 8, 64), dtype=torch.bfloat16, device="cuda")
-    w = torch.zeros((1, 64, 64), dtype=torch.bfloat16, device="cuda")     # E = 64
+    w = torch.zeros((1, 320, 64), dtype=torch.bfloat16, device="cuda")     # E = 320 > 256
     off = torch.tensor([0, 1], dtype=torch.int32, device="cuda")
     ri = torch.zeros(8, dtype=torch.int32, device="cuda")
     with pytest.raises(ev.EvictError) as e:

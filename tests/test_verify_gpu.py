@@ -170,6 +170,41 @@ def test_bad_links_flag_keep():
     assert torch.cuda.is_available()
 
 
+def test_orphan_slot_beats_bad_token():
+    """A tree with both an orphan slot and a bad token reports BAD_KEEP (the checks run in header
+    order: size/keep, then token, then prob), like the oracle's keep-before-token order."""
+    V = 256
+    P, Q, n, kb, off, tok, probs, ua, ub = _case(17, 4, 60, V, keep="all")
+    tok = tok.copy()
+    tok[2, 3] = V + 1                        # a kept node's token out of range
+
+    def cut(args):
+        nt = args["next_token"].clone()
+        nt[int(off[2])] = -1                 # tree 2: the root loses its child list -> orphan slots
+        args["next_token"] = nt
+
+    for greedy in (False, True):
+        g = _gpu(P, n, kb, tok, probs, ua, ub, V, greedy=greedy, mutate=cut)
+        st = g["status"].astype(np.int64) & 0xFFFFFFFF
+        assert st[2] == ov.TREE_BAD_KEEP, (greedy, st)
+        assert (st[[0, 1, 3]] == 0).all()
+
+
+def test_bad_bonus_entry_in_a_peer_cta():
+    """Batch 8 runs 8-CTA clusters per tree; a NaN at the last token of every row of trees 1 and 5
+    is summed by a peer CTA (chunk 39 of 40), which reports it to CTA 0 without touching CTA 0's
+    status word before the cluster barrier.  Status and outputs must equal the oracle."""
+    V = 20000
+    P, Q, n, kb, off, tok, probs, ua, ub = _case(18, 8, 60, V)
+    probs = probs.copy()
+    for b in (1, 5):
+        probs[off[b]:off[b + 1], V - 1] = np.nan
+    o = ov.verify_sample(P, kb, tok, probs, ua, ub, n_nodes=n, verify_offsets=off)
+    assert o["status"][1] == ov.TREE_BAD_PROB and o["status"][5] == ov.TREE_BAD_PROB
+    for exact in (False, True):
+        _compare(o, _gpu(P, n, kb, tok, probs, ua, ub, V, exact=exact))
+
+
 @pytest.mark.parametrize("exact", [False, True])
 def test_parity_threshold_on_a_cdf_boundary(exact):
     """Draws that land exactly on a CDF step (dyadic rows, u = 1/4, 1/2, 3/4, …): the fp64 fast
