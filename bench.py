@@ -2,12 +2,17 @@
 """EVICT hot-path benchmark (BASELINE.json metric: trees/s and µs per batch-64 selection;
 expert-union HBM GB/s vs B200 peak at 1/2/4/8 GPUs).
 
-Workload (BASELINE.json configs[4], "c5"): per rank, 1,000,000 synthetic EAGLE-3-shaped draft
+Workload (BASELINE.json configs[4], "c5"): the set of 1,000,000 synthetic EAGLE-3-shaped draft
 trees of 60 nodes (steps 6, topk 10) with Qwen3-30B-A3B-shaped routing (48 layers × 128 experts,
-top-8, uint8 ids: 23 GB), device-resident.  One step = one pass of the whole hot path over the
-rank's shard: the fused select → verify-tree build → expert-union launch (A1–A7), the batch
-statistics kernel (A9) and, for N > 1, the NCCL all-reduce of those statistics.  Trees are
-independent requests, so the shard is fixed per rank ("scaling": "weak").
+top-8, uint8 ids: 23 GB), sharded by request over the N ranks (rank r: tree ids
+[⌊rM/N⌋, ⌊(r+1)M/N⌋), generated on its GPU from (seed, tree id), device-resident).  One step =
+one pass of the whole hot path over the rank's shard: the fused select → verify-tree build →
+expert-union launch (A1–A7), the batch statistics kernel (A9) and, for N > 1, the NCCL
+all-reduce of those statistics.  The headline splits the fixed 1M-tree set ("scaling":
+"strong"); for N > 1 a weak-scaling sweep (1M trees per rank) is reported beside it.
+
+`python bench.py --gpus N` without a torchrun environment re-executes itself under
+torch.distributed.run with N local ranks (one per GPU, NCCL over NVLink).
 
 Timing: W warm-up steps, then K steps between a barrier + synchronize on both sides, timed
 with CUDA events on the launching stream, max over ranks.  Inputs (23 GB/rank) are far larger
@@ -42,7 +47,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--trees", type=int, default=1_000_000, help="trees per rank")
+    ap.add_argument("--trees", type=int, default=1_000_000,
+                    help="total trees (strong scaling: split over the ranks)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: --trees in total; weak: --trees per rank")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU check of the launcher, sharding and all-reduce (gloo, no kernels)")
     ap.add_argument("--id-format", default="u8", choices=["u8", "i32", "mask"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-extras", action="store_true", help="skip latency / variant sub-benchmarks")
@@ -213,7 +223,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "trees/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config_dict(args, world, S),
         "cpu_baseline": {"value": v, "unit": "trees/s", "cores": threads, "kind": "oracle",
                          "sample": sample},
@@ -223,10 +233,13 @@ def run_reference(args, rank, world):
     return 0
 
 
-def config_dict(args, world, trees=None):
+def config_dict(args, world, trees=None, total=None):
     return {"workload": "c5: EAGLE-3-shaped 60-node draft trees (steps 6, topk 10), "
                         "Qwen3-30B-A3B-shaped routing 48 layers x 128 experts top-8",
-            "trees_per_rank": trees or args.trees, "max_nodes": N_NODES, "layers": L_LAYERS,
+            "trees_total": total if total is not None else (
+                args.trees if args.scaling == "strong" else args.trees * world),
+            "trees_per_rank": trees or (args.trees if args.scaling == "weak" else
+                                        -(-args.trees // world)), "max_nodes": N_NODES, "layers": L_LAYERS,
             "experts": N_EXPERTS, "top_k": TOP_K, "id_format": args.id_format,
             "cost_table": "C(k)=10.47+0.0915*U(k)+0.15k ms (DESIGN.md §4)",
             "l2": "inputs >= 23 GB per rank >> 126 MB L2; no flush needed",
@@ -234,29 +247,48 @@ def config_dict(args, world, trees=None):
 
 
 # ------------------------------------------------------------------ native arm
-def cpu_baseline(args, k_star_mean):
+def cpu_baseline(args, k_star_mean, gpu_out=None, base=0):
     import numpy as np
 
     import gen
     import oracle
+    from oracle.parity import compare_select, compare_union, downstream_keep
     threads = os.cpu_count() or 1
     cost = gen.cost_table(N_NODES)
     pilot = 2000
-    P, Q, n = gen.trees(SEED, pilot, N_NODES, STEPS, TOPK, threads=threads)
-    ids = gen.routing(SEED, pilot, N_NODES, L_LAYERS, N_EXPERTS, TOP_K, threads=threads)
+    P, Q, n = gen.trees(SEED, pilot, N_NODES, STEPS, TOPK, tree_base=base, threads=threads)
+    ids = gen.routing(SEED, pilot, N_NODES, L_LAYERS, N_EXPERTS, TOP_K, tree_base=base, threads=threads)
     t0 = time.perf_counter()
     o = oracle.select(P, Q, cost, n_nodes=n, threads=threads)
     oracle.build_verify_tree(P, o["keep_bits"], n_nodes=n)
     oracle.expert_union(o["keep_bits"], ids, N_EXPERTS, n_nodes=n, threads=threads)
     per = (time.perf_counter() - t0) / pilot
     S = int(min(400_000, max(pilot, args.cpu_seconds / per)))
-    P, Q, n = gen.trees(SEED, S, N_NODES, STEPS, TOPK, threads=threads)
-    ids = gen.routing(SEED, S, N_NODES, L_LAYERS, N_EXPERTS, TOP_K, threads=threads)
+    P, Q, n = gen.trees(SEED, S, N_NODES, STEPS, TOPK, tree_base=base, threads=threads)
+    ids = gen.routing(SEED, S, N_NODES, L_LAYERS, N_EXPERTS, TOP_K, tree_base=base, threads=threads)
     t0 = time.perf_counter()
     o = oracle.select(P, Q, cost, n_nodes=n, threads=threads)
     oracle.build_verify_tree(P, o["keep_bits"], n_nodes=n)
-    oracle.expert_union(o["keep_bits"], ids, N_EXPERTS, n_nodes=n, threads=threads)
+    ou = oracle.expert_union(o["keep_bits"], ids, N_EXPERTS, n_nodes=n, threads=threads)
     dt = time.perf_counter() - t0
+    # parity of the GPU's outputs for the same trees (the bench's exact launch; SURVEY §5 counts)
+    parity = None
+    if gpu_out is not None:
+        m = min(S, len(gpu_out["k_star"]))
+        osub = {k: v[:m] for k, v in o.items()}
+        res, msgs = compare_select(osub, {k: gpu_out[k][:m] for k in ("k_star", "e_hat", "utility",
+                                                                      "keep_bits", "status")}, n_nodes=n[:m])
+        keep = downstream_keep(osub, {"k_star": gpu_out["k_star"][:m]})
+        ou2 = ou if (keep == o["keep_bits"][:m]).all() and m == S else oracle.expert_union(
+            keep, ids[:m], N_EXPERTS, n_nodes=n[:m], threads=threads)
+        um = compare_union({k: v[:m] for k, v in ou2.items()},
+                           {k: gpu_out[k][:m] for k in ("union_count", "union_total")})
+        parity = dict(res, trees=m, union_mismatch=len(um), first_mismatch=(msgs + um)[:1],
+                      rule="k*/keep bit-exact, e_hat/utility 1e-5 rel, ties per the oracle near-tie set; "
+                           "union counts bit-exact")
+    per_config = {}
+    for name in ("toy", "c2", "c3", "c4"):
+        per_config[name] = _oracle_config_ms(gen, oracle, name, threads)
     # one-thread rate on the first 20,000 of the same trees (both are reported)
     S1 = min(S, 20_000)
     t0 = time.perf_counter()
@@ -271,16 +303,42 @@ def cpu_baseline(args, k_star_mean):
     except OSError:
         pass
     return {"value": S / dt, "unit": "trees/s", "cores": threads, "kind": "oracle",
-            "one_thread_value": S1 / dt1, "cpu_model": model,
+            "one_thread_value": S1 / dt1, "cpu_model": model, "parity": parity,
+            "per_config_ms_per_batch": per_config,
             "sample": f"first {S} trees of rank 0's c5 shard (seed {SEED}); oracle select+build+"
                       f"union (C, fp64 sums) on {threads} host threads (one_thread_value: first {S1} "
                       f"on 1 thread); generation excluded"}
 
 
-def latency_b64(ev, torch, gen, N=60, steps=6, topk=10, seed=4, replays=2000):
-    """µs per batch-64 selection (select only, and fused select+build+union), CUDA-graph replay."""
+def _oracle_config_ms(gen, oracle, name, threads):
+    """Oracle select+build+union ms per batch of a BASELINE config (C1 toy / C2 / C3 / C4),
+    median of 5."""
     import numpy as np
-    B = 64
+    c = gen.CONFIGS[name]
+    if name == "toy":
+        P, Q, n = gen.TOY_PARENT[None], gen.TOY_Q[None], np.array([8], np.int32)
+        cost = gen.TOY_COST
+        ids = gen.TOY_ROUTING[None]
+        E = c["E"]
+    else:
+        P, Q, n = gen.trees(c["seed"], c["B"], c["N"], c["steps"], c["topk"])
+        cost = gen.cost_table(c["N"])
+        ids = gen.routing(c["seed"], c["B"], c["N"], c["L"], c["E"], c["K"])
+        E = c["E"]
+    ts = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        o = oracle.select(P, Q, cost, n_nodes=n, threads=threads)
+        oracle.build_verify_tree(P, o["keep_bits"], n_nodes=n)
+        oracle.expert_union(o["keep_bits"], ids, E, n_nodes=n, threads=threads)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    return {"B": int(P.shape[0]), "N": int(P.shape[1]), "ms": float(np.median(ts))}
+
+
+def latency(ev, torch, gen, B=64, N=60, steps=6, topk=10, seed=4, replays=2000):
+    """µs per batch-B selection (select only, and fused select+build+union), CUDA-graph replay.
+    B = 64 is the north_star latency point; B = 1 the paper's serving setting."""
+    import numpy as np
     P, Q, n = gen.trees(seed, B, N, steps, topk)
     cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
     tP, tQ, tn, tc = cu(P), cu(Q), cu(n), cu(gen.cost_table(N))
@@ -321,7 +379,7 @@ def latency_b64(ev, torch, gen, N=60, steps=6, topk=10, seed=4, replays=2000):
                 g.replay()
             e1.record(s)
         e1.synchronize()
-        out[f"{name}_b64_n{N}_us"] = e0.elapsed_time(e1) * 1e3 / replays
+        out[f"{name}_b{B}_n{N}_us"] = e0.elapsed_time(e1) * 1e3 / replays
         # per-replay device times (SURVEY §8(d) latency): p50 / p99 over 1000 replays
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(1000)]
         with torch.cuda.stream(s):
@@ -331,8 +389,8 @@ def latency_b64(ev, torch, gen, N=60, steps=6, topk=10, seed=4, replays=2000):
                 b.record(s)
         s.synchronize()
         t = np.sort([a.elapsed_time(b) * 1e3 for a, b in evs])
-        out[f"{name}_b64_n{N}_p50_us"] = float(t[len(t) // 2])
-        out[f"{name}_b64_n{N}_p99_us"] = float(t[int(len(t) * 0.99)])
+        out[f"{name}_b{B}_n{N}_p50_us"] = float(t[len(t) // 2])
+        out[f"{name}_b{B}_n{N}_p99_us"] = float(t[int(len(t) * 0.99)])
     return out
 
 
@@ -674,20 +732,8 @@ def router_bench(ev, gen, torch, stream):
     return res
 
 
-def run_native(args, rank, world, local_rank):
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-
-    import gen
-    import paper_2605_00342_b200 as ev
-    from paper_2605_00342_b200.dist import allreduce_stats, max_over_ranks, shard
-
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    ev.lib()
-    base, M = shard(rank, world, args.trees)
-    # ---- device-resident synthetic inputs (generation excluded from timing)
+def make_shard(args, ev, gen, torch, dev, base, M):
+    """Device-resident inputs of tree ids [base, base + M) (generation excluded from timing)."""
     P, Q, n = gen.trees_cuda(SEED, M, N_NODES, STEPS, TOPK, tree_base=base)
     cost = torch.from_numpy(gen.cost_table(N_NODES)).to(dev)
     ids8 = gen.routing_cuda(SEED, M, N_NODES, L_LAYERS, N_EXPERTS, TOP_K, tree_base=base)
@@ -700,17 +746,23 @@ def run_native(args, rank, world, local_rank):
         ids, id_bytes = gen.ids_to_mask_cuda(ids8, N_EXPERTS), 8
         del ids8
     torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
+    return P, Q, n, cost, ids, id_bytes
+
+
+def timed_sweep(args, ev, torch, dist, dev, stream, P, Q, n, cost, ids, M, world, local_rank, K, W):
+    """W warm-up + K timed steps (fused A1–A7 launch, A9 stats, NCCL all-reduce of the stats)
+    between barrier + synchronize; CUDA events on the launching stream; max over ranks."""
+    from paper_2605_00342_b200.dist import allreduce_stats, max_over_ranks
     call = ev.FusedCall(P, Q, cost, ids, N_EXPERTS, n_nodes=n)
     bufs = call.buffers.t
     stats_t = torch.empty(6 + N_NODES + L_LAYERS, dtype=torch.int64, device=dev)
     dstats_t = torch.empty(2, dtype=torch.float64, device=dev)
 
-    def stats_call():
+    def stats_call(st, dst):
         rc = ev.lib().evict_batch_stats(M, N_NODES, L_LAYERS, ev._p(n), ev._p(bufs["k_star"]),
                                         ev._p(bufs["e_hat"]), ev._p(bufs["utility"]),
                                         ev._p(bufs["union_count"]), ev._p(bufs["status"]),
-                                        ev._p(stats_t), ev._p(dstats_t), ev._stream(stream))
+                                        ev._p(st), ev._p(dst), ev._stream(stream))
         assert rc == 0
 
     def step(ev0=None, ev1=None):
@@ -719,15 +771,14 @@ def run_native(args, rank, world, local_rank):
         call(stream)
         if ev1 is not None:
             ev1.record(stream)
-        stats_call()
+        stats_call(stats_t, dstats_t)
         allreduce_stats(stats_t, dstats_t)
 
-    for _ in range(max(3, args.warmup)):
+    for _ in range(max(3, W)):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    K = args.steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clk = ClockSampler(local_rank)
@@ -749,19 +800,39 @@ def run_native(args, rank, world, local_rank):
     elapsed_ms = t0.elapsed_time(t1)
     kern_ms = sum(a.elapsed_time(b) for a, b in evs) / K
     tm = max_over_ranks(torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev))
-    elapsed_ms, kern_ms = float(tm[0]), float(tm[1])
-    st = stats_t.cpu().numpy()
     # single-rank stats of this shard (the all-reduced vector sums every rank)
     local = torch.empty_like(stats_t)
     ldst = torch.empty_like(dstats_t)
-    rc = ev.lib().evict_batch_stats(M, N_NODES, L_LAYERS, ev._p(n), ev._p(bufs["k_star"]),
-                                    ev._p(bufs["e_hat"]), ev._p(bufs["utility"]),
-                                    ev._p(bufs["union_count"]), ev._p(bufs["status"]),
-                                    ev._p(local), ev._p(ldst), ev._stream(stream))
-    assert rc == 0
-    lst = local.cpu().numpy()
-    total_trees = M * world
-    value = total_trees * K / (elapsed_ms / 1e3)
+    stats_call(local, ldst)
+    return dict(elapsed_ms=float(tm[0]), kern_ms=float(tm[1]), clocks=clocks, bufs=bufs,
+                stats=stats_t.cpu().numpy(), local=local.cpu().numpy())
+
+
+def run_native(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import gen
+    import paper_2605_00342_b200 as ev
+    from paper_2605_00342_b200.dist import shard
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    ev.lib()
+    if args.scaling == "strong":
+        base, M = shard(rank, world, 0, total=args.trees)
+        total = args.trees
+    else:
+        base, M = shard(rank, world, args.trees)
+        total = args.trees * world
+    P, Q, n, cost, ids, id_bytes = make_shard(args, ev, gen, torch, dev, base, M)
+    stream = torch.cuda.current_stream()
+    K = args.steps
+    sw = timed_sweep(args, ev, torch, dist, dev, stream, P, Q, n, cost, ids, M, world, local_rank, K,
+                     args.warmup)
+    elapsed_ms, kern_ms, st, lst = sw["elapsed_ms"], sw["kern_ms"], sw["stats"], sw["local"]
+    bufs = sw["bufs"]
+    value = total * K / (elapsed_ms / 1e3)
     abytes, parts = algorithmic_bytes(int(lst[2]), int(lst[1]), M, id_bytes,
                                       id_format=args.id_format)
     peak, peak_kind = hbm_peak()
@@ -776,8 +847,8 @@ def run_native(args, rank, world, local_rank):
     result = {
         "metric": METRIC, "value": value, "unit": "trees/s", "n_gpus": world, "steps": K,
         "warmup": max(3, args.warmup), "ms_per_step": elapsed_ms / K, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": config_dict(args, world),
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(args, world, M, total),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_fused (select+build+union)", "peak_kind": peak_kind,
@@ -788,8 +859,21 @@ def run_native(args, rank, world, local_rank):
         "k_star_mean": float(lst[1]) / max(1, M - int(lst[4])),
         "union_mean_per_layer": float(lst[3]) / max(1, (M - int(lst[4])) * L_LAYERS),
         "stats_allreduced_trees": int(st[0]),
-        "clocks": clocks,
+        "shard": {"rank0_tree_ids": [base, base + M], "collective": "NCCL all_reduce(SUM) of the "
+                  "A9 stats vector + all_reduce(MAX) of the elapsed time" if world > 1 else None},
+        "clocks": sw["clocks"],
     }
+    if world > 1 and not args.no_extras and args.scaling == "strong":
+        # weak scaling beside the headline: 1M trees per rank (tree ids [r·1M, (r+1)·1M))
+        wb, wM = shard(rank, world, args.trees)
+        wP, wQ, wn, wc, wi, _ = make_shard(args, ev, gen, torch, dev, wb, wM)
+        ws = timed_sweep(args, ev, torch, dist, dev, stream, wP, wQ, wn, wc, wi, wM, world, local_rank,
+                         K, args.warmup)
+        result["weak_scaling"] = {"value": wM * world * K / (ws["elapsed_ms"] / 1e3), "unit": "trees/s",
+                                  "trees_per_rank": wM, "ms_per_step": ws["elapsed_ms"] / K,
+                                  "kernel_ms": ws["kern_ms"], "stats_allreduced_trees": int(ws["stats"][0])}
+        del wP, wQ, wn, wc, wi, ws
+        torch.cuda.empty_cache()
     # ---- end-to-end through the public API with host buffers (rank-local)
     result["e2e"] = e2e(args, ev, torch, P, Q, n, cost, ids, M, world, stream)
     if not args.no_extras and args.id_format == "u8":
@@ -828,13 +912,19 @@ def run_native(args, rank, world, local_rank):
         except Exception as e:  # pragma: no cover
             result["verify"] = {"error": repr(e)}
         try:
-            result["latency"] = latency_b64(ev, torch, gen)
-            result["latency"].update({k.replace("n60", "n128"): v for k, v in
-                                      latency_b64(ev, torch, gen, N=128, steps=8, topk=10).items()})
+            lat = {}
+            for B, N, steps, topk in ((64, 60, 6, 10), (1, 60, 6, 10), (64, 128, 8, 10)):
+                lat.update(latency(ev, torch, gen, B=B, N=N, steps=steps, topk=topk))
+            result["latency"] = lat
         except Exception as e:  # pragma: no cover
             result["latency"] = {"error": repr(e)}
     if rank == 0:
-        result["cpu_baseline"] = cpu_baseline(args, result["k_star_mean"])
+        # the oracle leg: timed on a bounded sample of rank 0's shard, and its outputs compared with
+        # the GPU's for the same trees (outside every timed region)
+        S_par = min(M, 20_000)
+        gpu_out = {k: bufs[k][:S_par].cpu().numpy() for k in ("k_star", "e_hat", "utility", "keep_bits",
+                                                             "union_count", "union_total", "status")}
+        result["cpu_baseline"] = cpu_baseline(args, result["k_star_mean"], gpu_out, base)
         print(json.dumps(result), flush=True)
     return 0
 
@@ -938,17 +1028,79 @@ def _slice_bufs(b, m, ev):
     return v
 
 
+def spawn(args):
+    """`--gpus N` outside torchrun: re-execute this script under torch.distributed.run with N local
+    ranks (the driver's own launch line); rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    if not args.dry_run:
+        # communicator init lines (comm_nranks) in the log, so the world size is checkable
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def dry_run(args, rank, world):
+    """CPU check of the multi-rank plumbing (gloo): every rank takes its shard of the tree ids,
+    the per-rank counters are summed by all_reduce and the elapsed time max-reduced, exactly the
+    collectives of the GPU step.  No kernels run; the line says so."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_00342_b200.dist import allreduce_stats, max_over_ranks, shard
+    if args.scaling == "strong":
+        base, M = shard(rank, world, 0, total=args.trees)
+    else:
+        base, M = shard(rank, world, args.trees)
+    ids = torch.arange(base, base + M, dtype=torch.int64)
+    st = torch.tensor([M, int(ids.sum()), int((ids * ids).sum())], dtype=torch.int64)
+    dst = torch.tensor([float(M), 0.0], dtype=torch.float64)
+    t0 = time.perf_counter()
+    allreduce_stats(st, dst)
+    el = max_over_ranks(torch.tensor([time.perf_counter() - t0], dtype=torch.float64))
+    shards = [None] * world
+    if world > 1:
+        dist.all_gather_object(shards, [base, M])
+    else:
+        shards = [[base, M]]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "scaling": args.scaling,
+                          "backend": dist.get_backend() if world > 1 else None,
+                          "shards": shards, "trees": int(st[0]), "id_sum": int(st[1]),
+                          "id_sq_sum": int(st[2]), "elapsed_s": float(el[0]),
+                          "config": config_dict(args, world, M)}), flush=True)
+    return 0
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
     rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))
+    world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus and rank == 0:
+        print(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}; reporting n_gpus={world}", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     import torch
     import torch.distributed as dist
+    if args.dry_run:
+        if world > 1:
+            dist.init_process_group("gloo")
+        try:
+            return dry_run(args, rank, world)
+        finally:
+            if world > 1:
+                dist.destroy_process_group()
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        print(f"bench: rank {rank}/{world} on cuda:{local_rank}, backend {dist.get_backend()}, "
+              f"comm_nranks {dist.get_world_size()}", file=sys.stderr, flush=True)
     try:
         return run_native(args, rank, world, local_rank)
     finally:

@@ -20,6 +20,10 @@ import torch
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libevict.so")
+# kernel A/B experiments only: EVICT_LIB_VARIANT=x loads libevict_x.so (built by
+# `python -m paper_2605_00342_b200.build --variant x -D...`); the product build is libevict.so
+if os.environ.get("EVICT_LIB_VARIANT"):
+    LIB_PATH = os.path.join(PKG, f"libevict_{os.environ['EVICT_LIB_VARIANT']}.so")
 
 EVICT_OK, EVICT_ERR_INVALID_ARG, EVICT_ERR_UNSUPPORTED, EVICT_ERR_CUDA = 0, 1, 2, 3
 TREE_BAD_SIZE, TREE_BAD_PARENT, TREE_BAD_PROB = 0x01, 0x02, 0x04

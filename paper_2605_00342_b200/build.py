@@ -58,8 +58,19 @@ def _includes(path, seen=None):
     return seen
 
 
+VARIANT = [None, []]   # (name, extra -D flags): kernel A/B builds into build_<name>/, libevict_<name>.so
+
+
+def _objdir():
+    return OBJ if VARIANT[0] is None else OBJ + "_" + VARIANT[0]
+
+
+def _lib():
+    return LIB if VARIANT[0] is None else LIB.replace("libevict.so", f"libevict_{VARIANT[0]}.so")
+
+
 def _obj(src):
-    return os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+    return os.path.join(_objdir(), os.path.basename(src).replace(".cu", ".o"))
 
 
 def _obj_stale(src):
@@ -71,12 +82,12 @@ def _obj_stale(src):
 
 
 def _compile(src):
-    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(_objdir(), exist_ok=True)
     obj = _obj(src)
     if not FORCE[0] and not _obj_stale(src):
         return obj
     log = obj.replace(".o", ".ptxas.log")
-    cmd = ["nvcc", *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+    cmd = ["nvcc", *ARCH, *NVCC_FLAGS, *VARIANT[1], "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     with open(log, "w") as f:
         f.write(r.stdout + r.stderr)
@@ -89,18 +100,21 @@ FORCE = [False]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+    if VARIANT[0] is None and not force and not stale():
         return LIB
     FORCE[0] = force
     srcs = sources()
     with ThreadPoolExecutor(max(1, min(len(srcs), os.cpu_count() or 4))) as ex:
         objs = list(ex.map(_compile, srcs))
-    cmd = ["nvcc", *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lcuda"]
+    cmd = ["nvcc", *ARCH, "-shared", "-o", _lib(), *objs, "-lcudart", "-lcuda"]
     subprocess.check_call(cmd)
     if verbose:
-        print(f"built {LIB}", file=sys.stderr)
-    return LIB
+        print(f"built {_lib()}", file=sys.stderr)
+    return _lib()
 
 
 if __name__ == "__main__":
+    if "--variant" in sys.argv:
+        VARIANT[0] = sys.argv[sys.argv.index("--variant") + 1]
+        VARIANT[1] = [a for a in sys.argv if a.startswith("-D")]
     build(force="--force" in sys.argv, verbose=True)

@@ -86,8 +86,9 @@ const char *evict_status_string(evict_status_t s)
 size_t evict_workspace_bytes(int32_t batch)
 {
     if (batch < 1) return 0;
-    // one state word per tile of the finer of the two tilings (k_fused: 4-tree warp tiles)
-    const int tt = kTileTrees < kFusedTileTrees ? kTileTrees : kFusedTileTrees;
+    // one state word per tile of the finest tiling: k_fused takes one-tree warp tiles up to
+    // kFusedSmallBatch trees (serving batches), 4-tree tiles above; k_build 8-tree CTA tiles
+    const int tt = batch <= kFusedSmallBatch ? 1 : (kTileTrees < kFusedTileTrees ? kTileTrees : kFusedTileTrees);
     const size_t ntiles = ((size_t)batch + tt - 1) / tt;
     return 8 * (1 + ntiles);
 }
@@ -214,7 +215,8 @@ evict_status_t evict_select_build_union_policy(const evict_trees_t *trees, const
     }
     if (!dev_info().ok) return EVICT_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
-    const int ntiles = (trees->batch + kFusedTileTrees - 1) / kFusedTileTrees;
+    const int tt = trees->batch <= kFusedSmallBatch ? 1 : kFusedTileTrees;
+    const int ntiles = (trees->batch + tt - 1) / tt;
     if (cudaMemsetAsync(workspace, 0, 8 * (1 + (size_t)ntiles), s) != cudaSuccess)
         return EVICT_ERR_CUDA;
     uint64_t *ws = (uint64_t *)workspace;
@@ -223,3 +225,4 @@ evict_status_t evict_select_build_union_policy(const evict_trees_t *trees, const
 }
 
 }  // extern "C"
+

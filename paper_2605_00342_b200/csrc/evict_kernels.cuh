@@ -281,8 +281,55 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(evict_trees_t tr, const u
 //   C   verify-tree emit (A6) at the packed offsets.
 // Predecessor tiles always belong to warps that took their ticket earlier and
 // are resident, so the look-back cannot deadlock.
-constexpr int kWT = 4;                 // trees per warp tile
-constexpr int kTile = kWarps * kWT;    // records per CTA
+#ifdef EVICT_PHASE_TIMING
+// profiling variant only: per-phase SM cycles of k_fused summed over warps (lane 0)
+static __device__ unsigned long long g_phase_cycles[8];   // per translation unit
+#define EVICT_PHASE(i)                                                                     \
+    do {                                                                                   \
+        const long long now_ = clock64();                                                  \
+        if (lane == 0) atomicAdd(&g_phase_cycles[i], (unsigned long long)(now_ - ph_t));   \
+        ph_t = now_;                                                                       \
+    } while (0)
+#else
+#define EVICT_PHASE(i) do {} while (0)
+#endif
+constexpr int kWT = 4;                 // trees per warp tile (throughput batches)
+constexpr int kSmallBatch = 2048;      // up to here (serving batches, LEAN path): one tree per warp
+                                       // tile, so batch 64 spreads over 64 warps instead of 16
+
+// Warp-level decoupled look-back for tile `tile` (lane j reads the state of tile end − 1 − j per
+// round).  WAIT: re-poll unpublished predecessors until the walk ends; otherwise give up (return
+// false, prefix untouched) at the first unpublished predecessor or after kEarlyRounds rounds.
+// On success the tile's inclusive prefix (prefix + agg) is published and prefix holds the sum of
+// every predecessor's count.
+constexpr int kEarlyRounds = 4;
+template <bool WAIT>
+__device__ __forceinline__ bool lookback_walk(int tile, uint64_t *states, int agg, unsigned &prefix, int lane)
+{
+    unsigned acc = 0;
+    int end = tile, rounds = 0;
+    while (true) {
+        const int j = end - 1 - lane;
+        const uint64_t sv = j >= 0 ? ld_acquire(states + j) : kInc;
+        const unsigned flag = (unsigned)(sv >> 62);
+        const unsigned inc_mask = __ballot_sync(kFull, flag == 2);
+        const unsigned zero_mask = __ballot_sync(kFull, flag == 0);
+        const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
+        const unsigned before = first_inc == 32 ? kFull : ((1u << first_inc) - 1u);
+        if (zero_mask & before) {
+            if (!WAIT) return false;
+            continue;
+        }
+        const unsigned v = lane <= first_inc ? (unsigned)(sv & kValMask) : 0u;
+        acc += __reduce_add_sync(kFull, v);
+        if (first_inc < 32) break;
+        end -= 32;
+        if (!WAIT && ++rounds >= kEarlyRounds) return false;
+    }
+    if (lane == 0) st_release(states + tile, kInc | (uint64_t)(acc + (unsigned)agg));
+    prefix = acc;
+    return true;
+}
 
 template <int G>
 struct EmitRec {
@@ -321,18 +368,18 @@ __host__ __device__ inline size_t fused_scratch_bytes(int L, int E, bool flags)
     const size_t x = fused_scratch_fixed<G>();
     return align16(f > x ? f : x);
 }
-template <int G>
+template <int G, int WT = kWT>
 __host__ __device__ inline size_t fused_smem_bytes(int L, int E, bool flags)
 {
     return (size_t)kWarps * fused_scratch_bytes<G>(L, E, flags)          // scratch
-           + align16(sizeof(EmitRec<G>) * kTile)                         // records
+           + align16(sizeof(EmitRec<G>) * kWarps * WT)                   // records
            + (size_t)kWarps * grp::GShape<G>::TPW * grp::GShape<G>::NMAX; // ranks (order row)
 }
 
 // LEAN: the serving / bench configuration (u8 top-8 ids, E = 128 or 128 < E ≤ 256, no order row, no
 // union bit rows, no histogram) compiled without the other paths — with warps in
 // different phases the full kernel's code footprint thrashes the instruction cache.
-template <int NPL, int IDF, int KT, int EW, int CL, bool LEAN = false>
+template <int NPL, int IDF, int KT, int EW, int CL, bool LEAN = false, int WT = kWT>
 __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, const float *cost,
                                                        int cost_stride, evict_policy_t pol, evict_routing_t rt,
                                                        evict_fused_out_t out, uint64_t *ws,
@@ -343,7 +390,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     constexpr int TPW = grp::GShape<G>::TPW;
     constexpr int NMAX = grp::GShape<G>::NMAX;
     constexpr int W = grp::GShape<G>::W;
-    constexpr int PASSES = kWT / TPW;                // 1 (G=8) or 2 (G=16)
+    constexpr int PASSES = WT > TPW ? WT / TPW : 1;   // 1 (G=8, or WT = 1) or 2 (G=16, WT = 4)
     constexpr bool FLAGS = IDF == 1 || IDF == 4;
     extern __shared__ __align__(16) uint8_t dsm[];
     const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -354,8 +401,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     const bool do_union = out.union_count != nullptr;
     const size_t scratch = fused_scratch_bytes<G>(L, E, FLAGS && do_union);
     uint8_t *wscr = dsm + (size_t)warp * scratch;
-    EmitRec<G> *rec = reinterpret_cast<EmitRec<G> *>(dsm + (size_t)kWarps * scratch) + warp * kWT;
-    uint8_t *ranks = reinterpret_cast<uint8_t *>(dsm + (size_t)kWarps * scratch) + align16(sizeof(EmitRec<G>) * kTile);
+    EmitRec<G> *rec = reinterpret_cast<EmitRec<G> *>(dsm + (size_t)kWarps * scratch) + warp * WT;
+    uint8_t *ranks = reinterpret_cast<uint8_t *>(dsm + (size_t)kWarps * scratch) + align16(sizeof(EmitRec<G>) * kWarps * WT);
     uint8_t *rk = ranks + ((size_t)warp * TPW + gi) * NMAX;
     const int Epad = union_epad(E);
     unsigned *ticket = reinterpret_cast<unsigned *>(ws);
@@ -365,14 +412,17 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     tile = __shfl_sync(kFull, tile, 0);
     bool first = true;
     int epoch = 0;   // LEAN union marker window (tree_union_flags64)
+#ifdef EVICT_PHASE_TIMING
+    long long ph_t = clock64();
+#endif
     while (tile < ntiles) {
-        const int b0 = tile * kWT;
+        const int b0 = tile * WT;
         // ---------------- A1: select, sub-warp per tree
 #pragma unroll 1
         for (int pass = 0; pass < PASSES; pass++) {
             const int slot = pass * TPW + gi;
             const int b = b0 + slot;
-            const bool active = b < tr.batch;
+            const bool active = slot < WT && b < tr.batch;
             grp::GTree<G> t;
             grp::g_load<G>(t, tr.parent, tr.q, tr.n_nodes, b, N, active);
             float c[grp::NP];
@@ -386,7 +436,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             if (!LEAN && out.order) grp::g_rank_argmax<G>(t, rk, c, N, orow, prow, pol);   // kernel-uniform
             else grp::g_select_values<G>(t, c, N, prow, pol);
             const int k = t.kstar;
-            EmitRec<G> &er = rec[slot];
+            EmitRec<G> &er = rec[slot < WT ? slot : 0];
             if (active) {
                 if (g == 0) {
                     if (out.k_star) out.k_star[b] = t.kstar;
@@ -406,48 +456,36 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                     if (i < t.n && grp::bit_w<W>(t.keep, i)) er.klist[grp::popc_below_w<W>(t.keep, i)] = (uint8_t)i;
                 }
                 if (g == 0) { er.n = t.n; er.k = k; er.status = t.status; }
-            } else if (g == 0) {
+            } else if (g == 0 && slot < WT) {
                 er.k = 0;
             }
             __syncwarp();
         }
+        EVICT_PHASE(0);
         // ---------------- tile aggregate (lanes 0..3 = the tile's trees) + next ticket
-        const int cnt = lane < kWT ? rec[lane].k : 0;
+        const int cnt = lane < WT ? rec[lane].k : 0;
         int incl = cnt;
 #pragma unroll
-        for (int o = 1; o < kWT; o <<= 1) {
+        for (int o = 1; o < WT; o <<= 1) {
             const int v = __shfl_up_sync(kFull, incl, o);
             if (lane >= o) incl += v;
         }
-        const int agg = __shfl_sync(kFull, incl, kWT - 1);
+        const int agg = __shfl_sync(kFull, incl, WT - 1);
         int off_local = incl - cnt;
         if (lane == 0) st_release(states + tile, (tile == 0 ? kInc : kAgg) | (uint64_t)agg);
         int next = 0;
         if (lane == 0) next = (int)atomicAdd(ticket, 1u);
-        // ---------------- look-back for the tile prefix, right after the publish: predecessors
-        // publish their inclusive prefix just as early, so the walk ends within ~1 round (run
-        // after the union, it walked back over every warp still in its union: ~300 instructions
-        // per tree of polling at 24 warps/SM)
+        // ---------------- look-back, first attempt right after the publish: walk back over at most
+        // kEarlyRounds × 32 predecessor states without waiting; success publishes this tile's
+        // inclusive prefix now, so successors find one close by.  If a predecessor is still
+        // unpublished the attempt is dropped and the full look-back runs after the union (whose
+        // duration hides the wait).  (Only after the union, the walk crossed every tile still in
+        // its union — ~300 instructions of polling per tree; only before it, warps spun on
+        // predecessors still in their select: 2.5x slower.)
         unsigned prefix = 0;
-        if (tile > 0) {
-            int end = tile;
-            while (true) {
-                const int j = end - 1 - lane;
-                const uint64_t sv = j >= 0 ? ld_acquire(states + j) : kInc;
-                const unsigned flag = (unsigned)(sv >> 62);
-                const unsigned inc_mask = __ballot_sync(kFull, flag == 2);
-                const unsigned zero_mask = __ballot_sync(kFull, flag == 0);
-                const int first_inc = inc_mask ? __ffs(inc_mask) - 1 : 32;
-                const unsigned before = first_inc == 32 ? kFull : ((1u << first_inc) - 1u);
-                if (zero_mask & before) continue;
-                const unsigned v = lane <= first_inc ? (unsigned)(sv & kValMask) : 0u;
-                prefix += __reduce_add_sync(kFull, v);
-                if (first_inc < 32) break;
-                end -= 32;
-            }
-            if (lane == 0) st_release(states + tile, kInc | (uint64_t)(prefix + (unsigned)agg));
-        }
-        off_local += (int)prefix;
+        bool have = tile == 0;
+        if (!have) have = lookback_walk<false>(tile, states, agg, prefix, lane);
+        EVICT_PHASE(1);
         // ---------------- A2: expert union, one warp per tree
         if (do_union) {
             if constexpr (FLAGS) {
@@ -462,7 +500,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 first = false;
             }
 #pragma unroll 1
-            for (int slot = 0; slot < kWT; slot++) {
+            for (int slot = 0; slot < WT; slot++) {
                 const int b = b0 + slot;
                 if (b >= tr.batch) break;
                 EmitRec<G> &er = rec[slot];
@@ -483,16 +521,20 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 __syncwarp();
             }
         }
+        EVICT_PHASE(2);
+        if (!have) lookback_walk<true>(tile, states, agg, prefix, lane);
+        EVICT_PHASE(3);
+        off_local += (int)prefix;
         next = __shfl_sync(kFull, next, 0);
         // ---------------- C: verify-tree emit, sub-warp per tree
 #pragma unroll 1
         for (int pass = 0; pass < PASSES; pass++) {
             const int slot = pass * TPW + gi;
             const int b = b0 + slot;
-            const bool active = b < tr.batch;
-            const EmitRec<G> &er = rec[slot];
+            const bool active = slot < WT && b < tr.batch;
+            const EmitRec<G> &er = rec[slot < WT ? slot : 0];
             const int k = active ? er.k : 0;
-            const int off = __shfl_sync(kFull, off_local, slot);
+            const int off = __shfl_sync(kFull, off_local, slot < WT ? slot : 0);
             if (active && g == 0) {
                 if (out.status) out.status[b] = er.status;
                 if (out.verify_offsets) {
@@ -510,6 +552,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                            out.next_token, out.next_sibling, out.tree_mask);
             __syncwarp();
         }
+        EVICT_PHASE(4);
         tile = next;
     }
 }
@@ -629,19 +672,29 @@ struct UnionLauncher {
 
 template <int NPL, int IDF, int KT, int EW, int CL>
 struct FusedLauncher {
+    // the caller cleared 1 + batch tile states when batch ≤ kSmallBatch (else 1 + ⌈batch/4⌉)
     static evict_status_t run(const evict_trees_t *tr, const float *cost, int cs, evict_policy_t pol,
                               const evict_routing_t *rt, const evict_fused_out_t *o, uint64_t *ws,
-                              int ntiles, cudaStream_t s)
+                              int /*ntiles*/, cudaStream_t s)
     {
         auto kern = k_fused<NPL, IDF, KT, EW, CL, false>;
+        constexpr int G = NPL == 2 ? 8 : 16;
+        const bool flags = (IDF == 1 || IDF == 4) && o->union_count;
+        size_t dyn = fused_smem_bytes<G>(rt->num_layers, rt->num_experts, flags);
+        int wt = kWT;
         if constexpr (IDF == 1 && (EW == 2 || EW == 4)) {
             const bool shape = EW == 2 ? rt->num_experts == 128 : rt->num_experts > 128;
-            if (shape && !o->order && !o->union_bits && !o->expert_hist && o->union_count)
-                kern = k_fused<NPL, IDF, KT, EW, CL, true>;
+            if (shape && !o->order && !o->union_bits && !o->expert_hist && o->union_count) {
+                if (tr->batch <= kSmallBatch) {
+                    kern = k_fused<NPL, IDF, KT, EW, CL, true, 1>;
+                    dyn = fused_smem_bytes<G, 1>(rt->num_layers, rt->num_experts, flags);
+                    wt = 1;
+                } else {
+                    kern = k_fused<NPL, IDF, KT, EW, CL, true>;
+                }
+            }
         }
-        constexpr int G = NPL == 2 ? 8 : 16;
-        const size_t dyn = fused_smem_bytes<G>(rt->num_layers, rt->num_experts,
-                                               (IDF == 1 || IDF == 4) && o->union_count);
+        const int ntiles = (tr->batch + wt - 1) / wt;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         const int blocks = persistent_blocks(kern, ntiles, dyn);
         kern<<<blocks, kWarps * 32, dyn, s>>>(*tr, cost, cs, pol, *rt, *o, ws, ntiles);

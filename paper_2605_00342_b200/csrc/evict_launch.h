@@ -23,6 +23,7 @@
 namespace evict {
 constexpr int kTileTrees = 8;        // trees per CTA tile of k_build (= warps per CTA)
 constexpr int kFusedTileTrees = 4;   // trees per warp tile of k_fused
+constexpr int kFusedSmallBatch = 2048;   // k_fused LEAN takes one-tree tiles up to this batch
 int dev_sms();
 bool dev_supported();   // the current device is sm_100 (B200); else every entry point returns UNSUPPORTED
 template <int NPL> evict_status_t launch_select(EVICT_SELECT_ARGS);

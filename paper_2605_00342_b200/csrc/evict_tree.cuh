@@ -1159,8 +1159,8 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
             // node·row units (32-bit: node < 128, row ≤ 256) and a round 32 units
             const uint32_t *lane_u32 = reinterpret_cast<const uint32_t *>(ids) + (size_t)b * N * row + lane + 32 * RPP * pass;
             const int4 *lane_i4 = reinterpret_cast<const int4 *>(ids) + (size_t)b * N * row + lane + 32 * RPP * pass;
-            for (int j0 = 0; j0 < k; j0 += U) {
-                uint32_t v[U][RP][IDF];
+            // load a batch of U kept nodes' row parts (a batch past k re-reads node k-1)
+            auto load_batch = [&](int j0, uint32_t (&v)[U][RP][IDF]) {
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const uint32_t node = klist[min(j0 + u, k - 1)];
@@ -1180,6 +1180,8 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                         }
                     }
                 }
+            };
+            auto store_batch = [&](int j0, const uint32_t (&v)[U][RP][IDF]) {
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     if (j0 + u >= k) break;    // warp-uniform: a batch's tail re-read of node k-1 stores nothing
@@ -1207,6 +1209,28 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                         }
                     }
                 }
+            };
+#ifdef EVICT_UNION_PREFETCH
+            if constexpr (IDF == 1) {
+                // two register batches: batch j+1's loads are in flight while batch j stores
+                uint32_t va[U][RP][IDF], vb[U][RP][IDF];
+                load_batch(0, va);
+                for (int j0 = 0;;) {
+                    if (j0 + U < k) load_batch(j0 + U, vb);
+                    store_batch(j0, va);
+                    j0 += U;
+                    if (j0 >= k) break;
+                    if (j0 + U < k) load_batch(j0 + U, va);
+                    store_batch(j0, vb);
+                    j0 += U;
+                    if (j0 >= k) break;
+                }
+            } else
+#endif
+            for (int j0 = 0; j0 < k; j0 += U) {
+                uint32_t v[U][RP][IDF];
+                load_batch(j0, v);
+                store_batch(j0, v);
             }
         }
         __syncwarp();

@@ -428,13 +428,14 @@ def test_policy_rejects_bad_arguments(ev):
             ev.evict_select(P, Q, C, policy=bad)
 
 
+@pytest.mark.parametrize("B", [1, 64, 777, 5000])
 @pytest.mark.parametrize("name", ["c2", "ling", "c3", "c2_l56"])
-def test_fused_lean_path(ev, name):
+def test_fused_lean_path(ev, name, B):
     """The serving configuration (u8 top-8 ids, no order row, no bit rows, no histogram) runs the
     LEAN instantiation with marker-epoch flag blocks — E = 128 and the 256-expert layout; C3's
-    94 layers (R = 8: two flag passes, no marker epochs) and 56 layers (R = 4)."""
+    94 layers (R = 8: two flag passes, no marker epochs) and 56 layers (R = 4).  Batches up to
+    2048 take one-tree warp tiles (serving latency), larger ones 4-tree tiles."""
     c = _cfg(name)
-    B = 777
     N, L, E, K = c["N"], c["L"], c["E"], c["K"]
     P, Q, n = gen.trees(c["seed"] + 3, B, N, c["steps"], c["topk"])
     n[::5] = np.maximum(1, n[::5] // 3)
@@ -444,5 +445,8 @@ def test_fused_lean_path(ev, name):
     o = oracle.select(P, Q, cost, n_nodes=n, threads=8)
     res, msgs = compare_select(o, g, n_nodes=n)
     assert not msgs, msgs[:5]
-    ou = oracle.expert_union(downstream_keep(o, g), ids, E, n_nodes=n, threads=8)
+    keep = downstream_keep(o, g)
+    ou = oracle.expert_union(keep, ids, E, n_nodes=n, threads=8)
     assert not compare_union(ou, {k: v for k, v in g.items() if k in ("union_count", "union_total")})
+    ob = oracle.build_verify_tree(P, keep, n_nodes=n)
+    assert not compare_build(ob, {k: v for k, v in g.items() if k != "status"})

@@ -72,3 +72,30 @@ def test_shard_ranges():
     assert shard(3, 8, 1000) == (3000, 1000)
     parts = [shard(r, 3, 0, total=10) for r in range(3)]
     assert parts == [(0, 3), (3, 3), (6, 4)]
+
+
+@pytest.mark.parametrize("scaling,trees,world", [("strong", 1000, 2), ("strong", 1_000_001, 3), ("weak", 777, 2)])
+def test_bench_launcher_world2_gloo(scaling, trees, world):
+    """`bench.py --gpus N` with no torchrun environment spawns N ranks itself (torch.distributed.run
+    on 127.0.0.1); the dry run takes each rank's shard and runs the step's collectives on gloo.
+    The shards must tile the tree ids exactly once (strong: [0, trees); weak: trees per rank)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", str(world), "--dry-run",
+                        "--trees", str(trees), "--scaling", scaling], capture_output=True, text=True,
+                       timeout=240, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout            # rank 0 alone prints the line
+    out = json.loads(lines[0])
+    assert out["n_gpus"] == world and out["backend"] == "gloo"
+    total = trees if scaling == "strong" else trees * world
+    shards = out["shards"]
+    assert shards[0][0] == 0 and all(a + m == b for (a, m), (b, _) in zip(shards, shards[1:]))
+    assert sum(m for _, m in shards) == total == out["trees"]
+    assert max(m for _, m in shards) - min(m for _, m in shards) <= (1 if scaling == "strong" else 0)
+    assert out["id_sum"] == total * (total - 1) // 2          # every id once (all-reduced)
+    assert out["id_sq_sum"] == (total - 1) * total * (2 * total - 1) // 6
