@@ -203,6 +203,9 @@ evict_status_t evict_expert_union(const evict_trees_t *trees, const uint64_t *ke
  * evict_expert_union in ONE launch (the per-tree state stays on chip).
  * Semantics and outputs are exactly those of the three calls in sequence
  * (status is the OR of the three); any optional output may be NULL.
+ * workspace: evict_workspace_bytes(B) bytes, 8-byte aligned, cleared by the
+ * call (one state word per tile of the packed-offset scan: one tree per
+ * tile for B ≤ 2048 — serving batches, spread one tree per warp — else 4).
  * ------------------------------------------------------------------------- */
 typedef struct {
     /* select */

@@ -31,7 +31,8 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     assert lib.evict_abi_version() == 7
     lib.evict_workspace_bytes.restype = ctypes.c_size_t
-    assert lib.evict_workspace_bytes(64) == 8 * (1 + 16)   # one state word per 4-tree warp tile
+    assert lib.evict_workspace_bytes(64) == 8 * (1 + 64)   # serving batches: one state word per tree
+    assert lib.evict_workspace_bytes(4096) == 8 * (1 + 1024)   # above 2048: one per 4-tree warp tile
 
 
 def test_library_targets_sm100a_only():
