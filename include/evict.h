@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define EVICT_ABI_VERSION 7
+#define EVICT_ABI_VERSION 8
 #define EVICT_MAX_NODES 128   /* N ≤ 128 ⇒ W ≤ 2 mask words */
 #define EVICT_MAX_EXPERTS 256 /* Ling-flash-2.0 has 256 experts */
 #define EVICT_MAX_TOPK 16
@@ -190,7 +190,10 @@ typedef struct {
     int32_t num_experts; /* E ≥ 1, ≤ 256 */
     int32_t top_k;       /* K, 1 ≤ K ≤ min(E, 16) (ignored for EVICT_ID_MASK) */
     int32_t id_format;   /* EVICT_ID_U8 | EVICT_ID_I32 | EVICT_ID_MASK */
-    const void *ids;     /* see above */
+    const void *ids;     /* see above; device memory, or page-locked host memory mapped into the
+                            device address space (cudaHostAlloc under UVA): only the kept rows
+                            are read, so a host-resident routing table costs PCIe traffic for
+                            k*·L·K·s bytes per tree instead of a copy of every node's row */
 } evict_routing_t;
 
 evict_status_t evict_expert_union(const evict_trees_t *trees, const uint64_t *keep_bits,
@@ -230,6 +233,15 @@ typedef struct {
     uint64_t *union_bits;
     int64_t *expert_hist;
     uint32_t *status;
+    /* A9 (ABI 8): if non-NULL, the call also writes the batch statistics of
+     * evict_batch_stats over its own outputs (stats int64 [6 + N + L], dstats
+     * double [2]; both overwritten).  Requires k_star, e_hat, utility and status
+     * (and union_count when routing is given).  The serving configuration
+     * (u8 top-8 ids, E = 128, L ≤ 64, no order / bit rows / histogram)
+     * accumulates them inside the fused launch; other configurations run the
+     * statistics kernel after it. */
+    int64_t *stats;
+    double *dstats;
 } evict_fused_out_t;
 
 evict_status_t evict_select_build_union(const evict_trees_t *trees, const float *cost,

@@ -76,7 +76,7 @@ class _Router(ctypes.Structure):
 _OUT_FIELDS = ["k_star", "e_hat", "utility", "keep_bits", "order", "prefix_sums", "pos_offset",
                "verify_offsets", "kept_index", "retrieve_index", "positions", "next_token",
                "next_sibling", "tree_mask", "union_count", "union_total", "union_bits",
-               "expert_hist", "status"]
+               "expert_hist", "status", "stats", "dstats"]
 
 
 class _FusedOut(ctypes.Structure):
@@ -227,7 +227,9 @@ def evict_build_verify_tree(parent, keep_bits, n_nodes=None, pos_offset=None, q=
 def _routing(ids, num_experts, id_format=None):
     if id_format is None:
         id_format = {torch.uint8: ID_U8, torch.int32: ID_I32, torch.int64: ID_MASK}[ids.dtype]
-    assert ids.is_cuda and ids.is_contiguous()
+    # device memory, or page-locked host memory mapped into the device address space (UVA): the
+    # union then reads only the kept rows over PCIe (zero-copy)
+    assert (ids.is_cuda or ids.is_pinned()) and ids.is_contiguous()
     L = ids.shape[2]
     K = ids.shape[3] if id_format != ID_MASK else 0
     return _Routing(L, num_experts, K, id_format, _p(ids))
@@ -259,7 +261,7 @@ def evict_expert_union(keep_bits, ids, num_experts, n_nodes=None, max_nodes=None
 class FusedBuffers:
     """Pre-allocated outputs of evict_select_build_union for a fixed batch shape."""
 
-    def __init__(self, B, N, L, E, device, full=True, with_bits=False, with_order=False):
+    def __init__(self, B, N, L, E, device, full=True, with_bits=False, with_order=False, with_stats=False):
         W = (N + 63) // 64
         EW = (E + 63) // 64
         cap = B * N
@@ -281,6 +283,9 @@ class FusedBuffers:
         if with_order:
             self.t["order"] = torch.empty((B, N), dtype=torch.int32, device=d)
             self.t["prefix_sums"] = torch.empty((B, N), dtype=torch.float32, device=d)
+        if with_stats:   # A9 over the call's outputs (evict_batch_stats layout), ABI 8
+            self.t["stats"] = torch.empty(6 + N + L, dtype=torch.int64, device=d)
+            self.t["dstats"] = torch.empty(2, dtype=torch.float64, device=d)
         self.workspace = new_workspace(B, d)
 
     def struct(self, pos_offset=None):

@@ -213,15 +213,39 @@ evict_status_t evict_select_build_union_policy(const evict_trees_t *trees, const
         if (rc) return rc;
         rt = routing;
     }
+    // A9 (ABI 8): statistics over the call's own outputs
+    const bool want_stats = out->stats || out->dstats;
+    if (want_stats && (!out->stats || !out->dstats || !out->k_star || !out->e_hat || !out->utility ||
+                       !out->status))
+        return EVICT_ERR_INVALID_ARG;
     if (!dev_info().ok) return EVICT_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     const int tt = trees->batch <= kFusedSmallBatch ? 1 : kFusedTileTrees;
     const int ntiles = (trees->batch + tt - 1) / tt;
     if (cudaMemsetAsync(workspace, 0, 8 * (1 + (size_t)ntiles), s) != cudaSuccess)
         return EVICT_ERR_CUDA;
+    // folded into the launch for the single-pass E = 128 serving union (k_fused kFold), else the
+    // statistics kernel runs after it
+    const int L = out->union_count ? rt->num_layers : 0;
+    const bool fold = want_stats && out->union_count && rt->id_format == EVICT_ID_U8 && rt->top_k == 8 &&
+                      rt->num_experts == 128 && L <= 64 && !out->order && !out->union_bits && !out->expert_hist;
+    evict_fused_out_t o = *out;
+    if (want_stats) {
+        if (!fold) {
+            o.stats = nullptr;
+            o.dstats = nullptr;
+        } else if (cudaMemsetAsync(out->stats, 0, sizeof(int64_t) * (6 + (size_t)trees->max_nodes + L), s) != cudaSuccess ||
+                   cudaMemsetAsync(out->dstats, 0, 2 * sizeof(double), s) != cudaSuccess) {
+            return EVICT_ERR_CUDA;
+        }
+    }
     uint64_t *ws = (uint64_t *)workspace;
-    if (wide(trees->max_nodes)) return launch_fused<4>(trees, cost, (int)cost_stride, pol, rt, out, ws, ntiles, s);
-    return launch_fused<2>(trees, cost, (int)cost_stride, pol, rt, out, ws, ntiles, s);
+    rc = wide(trees->max_nodes) ? launch_fused<4>(trees, cost, (int)cost_stride, pol, rt, &o, ws, ntiles, s)
+                                : launch_fused<2>(trees, cost, (int)cost_stride, pol, rt, &o, ws, ntiles, s);
+    if (rc || !want_stats || fold) return rc;
+    return evict_batch_stats(trees->batch, trees->max_nodes, L, trees->n_nodes, out->k_star, out->e_hat,
+                             out->utility, L ? out->union_count : nullptr, out->status, out->stats,
+                             out->dstats, stream);
 }
 
 }  // extern "C"

@@ -340,7 +340,18 @@ struct EmitRec {
     alignas(8) uint8_t klist[NMAX];   // kept nodes, ascending (slot order), built once in A1
     int n, k;
     uint32_t status;
+    float ehat, util;                 // for the folded A9 statistics
 };
+
+// Folded A9 statistics (LEAN, E = 128, L ≤ 64): per-CTA accumulators at the end of the dynamic
+// shared memory, flushed to the global stats vector (evict_batch_stats layout) when the CTA ends.
+struct FusedStats {
+    unsigned sc[kWarps][4];     // per warp (no contention): trees, Σk*, Σn, errored trees
+    double d[kWarps][2];        // per warp: Σe_hat, Σutility (status 0)
+    unsigned hist[129];         // k* histogram, bin 0 = errored trees
+    unsigned lay[64];           // Σ union_count per layer (status 0)
+};
+constexpr size_t kStatsSmem = (sizeof(FusedStats) + 15) & ~(size_t)15;
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
@@ -373,7 +384,8 @@ __host__ __device__ inline size_t fused_smem_bytes(int L, int E, bool flags)
 {
     return (size_t)kWarps * fused_scratch_bytes<G>(L, E, flags)          // scratch
            + align16(sizeof(EmitRec<G>) * kWarps * WT)                   // records
-           + (size_t)kWarps * grp::GShape<G>::TPW * grp::GShape<G>::NMAX; // ranks (order row)
+           + align16((size_t)kWarps * grp::GShape<G>::TPW * grp::GShape<G>::NMAX)  // ranks (order row)
+           + kStatsSmem;                                                  // folded A9 statistics
 }
 
 // LEAN: the serving / bench configuration (u8 top-8 ids, E = 128 or 128 < E ≤ 256, no order row, no
@@ -404,6 +416,19 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     EmitRec<G> *rec = reinterpret_cast<EmitRec<G> *>(dsm + (size_t)kWarps * scratch) + warp * WT;
     uint8_t *ranks = reinterpret_cast<uint8_t *>(dsm + (size_t)kWarps * scratch) + align16(sizeof(EmitRec<G>) * kWarps * WT);
     uint8_t *rk = ranks + ((size_t)warp * TPW + gi) * NMAX;
+    FusedStats *fs = reinterpret_cast<FusedStats *>(ranks + align16((size_t)kWarps * TPW * NMAX));
+    // A9 folded into the launch: the single-pass E = 128 LEAN union (the caller passes out.stats
+    // only for that configuration; it runs evict_batch_stats after the launch otherwise)
+    constexpr bool kFold = LEAN && EW == 2 && CL <= 4;
+    const bool fstats = kFold && out.stats != nullptr;
+    uint32_t lsum[2] = {0u, 0u};
+    if constexpr (kFold) {
+        if (fstats) {
+            uint32_t *z = reinterpret_cast<uint32_t *>(fs);
+            for (int i = threadIdx.x; i < (int)(sizeof(FusedStats) / 4); i += blockDim.x) z[i] = 0u;
+            __syncthreads();
+        }
+    }
     const int Epad = union_epad(E);
     unsigned *ticket = reinterpret_cast<unsigned *>(ws);
     uint64_t *states = ws + 1;
@@ -455,7 +480,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                     const int i = base + r;
                     if (i < t.n && grp::bit_w<W>(t.keep, i)) er.klist[grp::popc_below_w<W>(t.keep, i)] = (uint8_t)i;
                 }
-                if (g == 0) { er.n = t.n; er.k = k; er.status = t.status; }
+                if (g == 0) { er.n = t.n; er.k = k; er.status = t.status; er.ehat = t.ehat; er.util = t.util; }
             } else if (g == 0 && slot < WT) {
                 er.k = 0;
             }
@@ -505,10 +530,27 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 if (b >= tr.batch) break;
                 EmitRec<G> &er = rec[slot];
                 uint32_t st = er.status;
-                if constexpr (LEAN && EW == 2)
+                if constexpr (LEAN && EW == 2) {
                     tree_union_flags64<1, CL, true, false>(st, er.klist, er.k, b, N, L, E, rt.ids, wscr,
                                                            out.union_count, out.union_total, nullptr,
-                                                           &epoch);
+                                                           &epoch, fstats ? lsum : nullptr);
+                    if constexpr (kFold) {
+                        if (fstats && lane == 0) {
+                            unsigned *wsc = fs->sc[warp];
+                            wsc[0] += 1u;
+                            if (st) {
+                                wsc[3] += 1u;
+                                atomicAdd(&fs->hist[0], 1u);
+                            } else {
+                                wsc[1] += (unsigned)er.k;
+                                wsc[2] += (unsigned)er.n;
+                                fs->d[warp][0] += (double)er.ehat;
+                                fs->d[warp][1] += (double)er.util;
+                                atomicAdd(&fs->hist[er.k], 1u);
+                            }
+                        }
+                    }
+                }
                 else if constexpr (LEAN)   // 128 < E ≤ 256 (Ling-flash-2.0): 32-byte expert rows
                     tree_union_flags64<1, CL, false, false, true>(st, er.klist, er.k, b, N, L, E, rt.ids, wscr,
                                                                   out.union_count, out.union_total, nullptr,
@@ -555,7 +597,40 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
         EVICT_PHASE(4);
         tile = next;
     }
+    if constexpr (kFold) {
+        if (fstats) {
+            // per-lane layer sums (layers 16·(bsel + 2hb) + 4q + m, as in tree_union_flags64)
+            const int q = lane & 3, m = (lane >> 2) & 3, bsel = lane >> 4;
+#pragma unroll
+            for (int hb = 0; hb < 2; hb++) {
+                const int l = 16 * (bsel + 2 * hb) + 4 * q + m;
+                if (l < L && lsum[hb]) atomicAdd(&fs->lay[l], lsum[hb]);
+            }
+            __syncthreads();
+            unsigned long long *gs = reinterpret_cast<unsigned long long *>(out.stats);
+            if (threadIdx.x == 0) {
+                unsigned long long su = 0, sc[4] = {0ull, 0ull, 0ull, 0ull};
+                for (int l = 0; l < L; l++) su += fs->lay[l];
+                for (int w = 0; w < kWarps; w++)
+                    for (int i = 0; i < 4; i++) sc[i] += fs->sc[w][i];
+                if (sc[0]) atomicAdd(gs + 0, sc[0]);
+                if (sc[1]) atomicAdd(gs + 1, sc[1]);
+                if (sc[2]) atomicAdd(gs + 2, sc[2]);
+                if (su) atomicAdd(gs + 3, su);
+                if (sc[3]) atomicAdd(gs + 4, sc[3]);
+                double de = 0.0, du = 0.0;
+                for (int w = 0; w < kWarps; w++) { de += fs->d[w][0]; du += fs->d[w][1]; }
+                atomicAdd(out.dstats + 0, de);
+                atomicAdd(out.dstats + 1, du);
+            }
+            for (int i = threadIdx.x; i <= N; i += blockDim.x)
+                if (fs->hist[i]) atomicAdd(gs + 5 + i, (unsigned long long)fs->hist[i]);
+            for (int l = threadIdx.x; l < L; l += blockDim.x)
+                if (fs->lay[l]) atomicAdd(gs + 6 + N + l, (unsigned long long)fs->lay[l]);
+        }
+    }
 }
+
 
 // ------------------------------------------------------------ select (grouped)
 // evict_select: G lanes per tree, 32/G trees per warp, 4 warps per CTA (small

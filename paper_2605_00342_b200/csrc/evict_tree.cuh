@@ -1122,8 +1122,12 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                                                    int b, int N, int L, int E, const void *__restrict__ ids,
                                                    uint8_t *flags, int32_t *__restrict__ union_count,
                                                    int32_t *__restrict__ union_total,
-                                                   uint64_t *__restrict__ union_bits, int *epoch = nullptr)
+                                                   uint64_t *__restrict__ union_bits, int *epoch = nullptr,
+                                                   uint32_t *lsum = nullptr)
 {
+    // lsum (single-pass E ≤ 128 layout only): lsum[hb] += this lane's count of layer
+    // 16·(bsel + 2·hb) + 4·(lane & 3) + (lane >> 2 & 3), bsel = lane >> 4 (A9 per-layer sums of
+    // good trees, folded into the fused launch)
     static_assert(IDF == 1 || IDF == 4, "flag union takes u8 or i32 ids");
     constexpr int RPP = W256 ? 2 : 4;                  // 16-layer rounds per pass
     constexpr int PASSES = (R + RPP - 1) / RPP;
@@ -1149,6 +1153,7 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
     uint32_t bad = 0;
     const bool run = status == 0;
     int tot = 0;
+    uint32_t lcnt[2] = {0u, 0u};
 #pragma unroll 1
     for (int pass = 0; pass < PASSES; pass++) {
         if (run) {
@@ -1313,6 +1318,7 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
                     const int cnt = (int)((x >> (8 * byte)) & 0xffu);
                     union_count[(size_t)b * L + l] = cnt;
                     tot += cnt;
+                    if (PASSES == 1 && lsum) lcnt[hb] = (uint32_t)cnt;
                 }
             }
             }
@@ -1331,6 +1337,7 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
         tot = 0;
     }
     __syncwarp();
+    if (lsum && run && !anybad) { lsum[0] += lcnt[0]; lsum[1] += lcnt[1]; }
     if (mark && run) *epoch = (ep + 1) & 3;   // the block was cleared when ep == 3
     tot = __reduce_add_sync(kFull, tot);
     if (union_total && lane == 0) union_total[b] = tot;

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     lib = ctypes.CDLL(ev.LIB_PATH)
     missing = [f for f in declared_functions() if not hasattr(lib, f)]
     assert not missing, missing
-    assert lib.evict_abi_version() == 7
+    assert lib.evict_abi_version() == 8
     lib.evict_workspace_bytes.restype = ctypes.c_size_t
     assert lib.evict_workspace_bytes(64) == 8 * (1 + 64)   # serving batches: one state word per tree
     assert lib.evict_workspace_bytes(4096) == 8 * (1 + 1024)   # above 2048: one per 4-tree warp tile

@@ -450,3 +450,46 @@ def test_fused_lean_path(ev, name, B):
     assert not compare_union(ou, {k: v for k, v in g.items() if k in ("union_count", "union_total")})
     ob = oracle.build_verify_tree(P, keep, n_nodes=n)
     assert not compare_build(ob, {k: v for k, v in g.items() if k != "status"})
+
+
+@pytest.mark.parametrize("name,fmt,B", [("c2", "u8", 777), ("c2", "u8", 5000), ("c2_l56", "u8", 3000),
+                                        ("c3", "u8", 500), ("c4_60", "i32", 300), ("ling", "u8", 300),
+                                        ("c4", "u8", 2100)])
+def test_fused_stats(ev, name, fmt, B):
+    """A9 statistics written by the fused call (ABI 8): folded into the launch for the E = 128,
+    L ≤ 64 serving union, the statistics kernel after it otherwise.  They must equal the oracle's
+    batch_stats over the call's own outputs (integers exact), errored trees included (NaN q,
+    an expert id ≥ E in a kept row)."""
+    c = _cfg(name)
+    N, L, E, K = c["N"], c["L"], c["E"], c["K"]
+    P, Q, n = gen.trees(c["seed"] + 5, B, N, c["steps"], c["topk"])
+    Q = Q.copy()
+    Q[3, 1] = np.nan                                      # BAD_PROB
+    ids = gen.routing(c["seed"] + 2, B, N, L, E, K, dtype=np.int32 if fmt == "i32" else np.uint8)
+    if E < 256:
+        ids[7, 0, 2, 1] = E + 3 if E + 3 < 256 else 255     # root is always kept: BAD_EXPERT
+    g = npy(ev.evict_select_build_union(T(P), T(Q), T(gen.cost_table(N)), T(ids), E, n_nodes=T(n),
+                                        with_stats=True))
+    assert g["status"][3] != 0 and (E == 256 or g["status"][7] != 0)
+    s, d = oracle.batch_stats(N, L, g["k_star"], g["e_hat"].astype(np.float64), g["utility"].astype(np.float64),
+                              g["union_count"], g["status"].astype(np.uint32), n_nodes=n)
+    assert (g["stats"] == s).all(), np.flatnonzero(g["stats"] != s)[:5]
+    assert np.allclose(g["dstats"], d, rtol=1e-9)
+
+
+@pytest.mark.parametrize("B", [300, 4000])
+def test_fused_reads_pinned_host_routing(ev, B):
+    """Routing ids in page-locked host memory (mapped, zero-copy): the fused call reads only the
+    kept rows over PCIe and must produce exactly the outputs of the device-resident call."""
+    import torch
+    c = gen.CONFIGS["c2"]
+    N, L, E, K = c["N"], c["L"], c["E"], c["K"]
+    P, Q, n = gen.trees(c["seed"] + 9, B, N, c["steps"], c["topk"])
+    ids = gen.routing(c["seed"] + 9, B, N, L, E, K)
+    host = torch.from_numpy(ids).pin_memory()
+    cost = T(gen.cost_table(N))
+    a = npy(ev.evict_select_build_union(T(P), T(Q), cost, T(ids), E, n_nodes=T(n)))
+    b = npy(ev.evict_select_build_union(T(P), T(Q), cost, host, E, n_nodes=T(n)))
+    torch.cuda.synchronize()
+    for k in ("k_star", "keep_bits", "union_count", "union_total", "status", "verify_offsets"):
+        assert (a[k] == b[k]).all(), k
