@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "evict.h"
@@ -58,6 +59,20 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar)
 __device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes)
 {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// arrive with a count (one thread completes `count` expected arrivals)
+__device__ __forceinline__ void mbar_arrive_cnt(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+// raise the phase's expected transaction bytes without arriving
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *m)
+{
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase)
 {
@@ -343,6 +358,80 @@ __device__ __forceinline__ Bits<NE> topk_warp_row(const float *lgrow, int K, int
     return r;
 }
 
+// TopK of one row by a whole warp as a truncated merge network: lane j holds experts j + 32q as
+// 64-bit keys (orderable logit bits << 32 | ~expert: larger key = larger logit, ties → smaller
+// expert), sorts its Q keys, then 5 xor-levels each merge two sorted KL-lists into the top KL of
+// their union (elementwise max of a and reversed b is bitonic; log2(KL) half-cleaner stages sort
+// it).  Every lane ends with the same top-KL; the first K are the TopK in rank order.
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m)
+{
+    const uint32_t lo = __shfl_xor_sync(0xffffffffu, (uint32_t)v, m);
+    const uint32_t hi = __shfl_xor_sync(0xffffffffu, (uint32_t)(v >> 32), m);
+    return ((uint64_t)hi << 32) | lo;
+}
+__device__ __forceinline__ uint64_t tkey(float v, int e)
+{
+    return ((uint64_t)f2ord(v) << 32) | (uint32_t)(~(uint32_t)e);
+}
+__device__ __forceinline__ void ce_desc(uint64_t &x, uint64_t &y)
+{
+    const uint64_t hi = x > y ? x : y, lo = x > y ? y : x;
+    x = hi;
+    y = lo;
+}
+template <int NE, int KL>
+__device__ __forceinline__ Bits<NE> topk_warp_merge(const float *lgrow, int K, int32_t *out, int lane)
+{
+    constexpr int Q = NE / 32;            // 4 (E ≤ 128) or 8 keys per lane
+    static_assert(Q <= KL, "a lane's keys fit its list");
+    uint64_t a[KL];
+#pragma unroll
+    for (int j = 0; j < KL; j++) a[j] = j < Q ? tkey(lgrow[lane + 32 * j], lane + 32 * j) : 0ull;
+    // local bitonic sort (descending) of the first Q keys; key 0 sorts below every real key
+#pragma unroll
+    for (int k = 2; k <= Q; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < Q; i++) {
+                const int ip = i ^ j;
+                if (ip > i) {
+                    if ((i & k) == 0) ce_desc(a[i], a[ip]);
+                    else ce_desc(a[ip], a[i]);
+                }
+            }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t c[KL];
+#pragma unroll
+        for (int j = 0; j < KL; j++) {
+            const uint64_t bj = shfl_xor_u64(a[KL - 1 - j], o);
+            c[j] = a[j] > bj ? a[j] : bj;
+        }
+#pragma unroll
+        for (int j = KL >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < KL; i++)
+                if ((i & j) == 0) ce_desc(c[i], c[i + j]);
+#pragma unroll
+        for (int j = 0; j < KL; j++) a[j] = c[j];
+    }
+    Bits<NE> r;
+#pragma unroll
+    for (int q = 0; q < NE / 32; q++) r.w[q] = 0u;
+#pragma unroll
+    for (int j = 0; j < KL; j++) {
+        if (j < K) {
+            const int e = (int)(~(uint32_t)a[j]);
+            const uint32_t bit = 1u << (e & 31);
+#pragma unroll
+            for (int q = 0; q < NE / 32; q++) r.w[q] |= (e >> 5) == q ? bit : 0u;
+            if (out && lane == j) out[j] = e;
+        }
+    }
+    return r;
+}
+
 struct Params {
     const uint16_t *hidden;        // bf16 [L][BNrows][d]
     const int32_t *verify_offsets; // [B+1]
@@ -367,9 +456,7 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
     constexpr int B_BYTES = b_bytes<NE>(), STAGE_BYTES = stage_bytes<NE>();
     static_assert(BM * LS * 4 <= STAGES * STAGE_BYTES, "logit staging must fit the operand ring");
     extern __shared__ uint8_t smem_raw[];
-    const int T = __ldg(p.verify_offsets + p.B);
     const int m0 = blockIdx.x * BM;
-    if (m0 >= T) return;                      // uniform per CTA, before any barrier
     const int l = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -383,22 +470,51 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
     auto Bs = [&](int s) { return base_u32 + s * STAGE_BYTES + A_BYTES; };
 
     const bool tr0 = p.trace && blockIdx.x == 0 && blockIdx.y == 0;
-    const int nrow = T - m0 < BM ? T - m0 : BM;   // valid rows of this tile
-    // sparse tiles gather their few hidden rows with TMA (gather4, one issuing thread);
-    // dense tiles use 128 cp.async producers (one TMA thread would serialise 32 gathers)
-    const bool sparse = nrow <= 32;
+    const int KB = p.d / BK;
+    // split z of S takes k-blocks [kb0, kb1); the S CTAs of a cluster share (tile, layer)
+    const int S = p.splits, z = blockIdx.z;
+    const int kb0 = (int)(((long)KB * z) / S), kb1 = (int)(((long)KB * (z + 1)) / S);
+    const int NKB = kb1 - kb0;
+    const int first = NKB < STAGES ? NKB : STAGES;
     if (tr0 && threadIdx.x == 0) {
         p.trace[250] = gtimer();
         p.trace[251] = p.splits;
     }
+    // full[s] expects NPROD + 1 arrivals: the W_g thread (arrive + its tx bytes) and the hidden
+    // rows — 128 cp.async producers (dense tiles) or one gather4 thread arriving with count NPROD
+    // after raising the tx bytes (sparse tiles); the same count either way, so the barriers and
+    // the first W_g loads go out before T (device-resident) is known
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
-            mbar_init(full0 + 8 * s, sparse ? 1 : NPROD + 1);
+            mbar_init(full0 + 8 * s, NPROD + 1);
             mbar_init(empty0 + 8 * s, 1);
         }
         mbar_init(tfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    __syncthreads();
+    if (warp == 5 && lane == 0) {
+        prefetch_tmap(&wmap);
+        prefetch_tmap(&hmap);
+        for (int i = 0; i < first; i++) {
+            mbar_arrive_tx(full0 + 8 * i, B_BYTES);
+            tma_load_3d(Bs(i), &wmap, full0 + 8 * i, (kb0 + i) * BK, 0, l);
+        }
+    }
+    const int T = __ldg(p.verify_offsets + p.B);
+    if (m0 >= T) {
+        // no rows in this tile: complete the issued stages' phases and wait for their W_g bytes
+        // (no TMA may land in an exited CTA)
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < first; s++) mbar_arrive_cnt(full0 + 8 * s, NPROD);
+            for (int s = 0; s < first; s++) mbar_wait(full0 + 8 * s, 0);
+        }
+        return;   // uniform per CTA; TMEM not yet allocated; no cluster peers (splits share T)
+    }
+    const int nrow = T - m0 < BM ? T - m0 : BM;   // valid rows of this tile
+    // sparse tiles gather their few hidden rows with TMA (gather4, one issuing thread);
+    // dense tiles use 128 cp.async producers (one TMA thread would serialise 32 gathers)
+    const bool sparse = nrow <= 32;
     if (warp == 4) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "n"(NE) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -411,11 +527,6 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    const int KB = p.d / BK;
-    // split z of S takes k-blocks [kb0, kb1); the S CTAs of a cluster share (tile, layer)
-    const int S = p.splits, z = blockIdx.z;
-    const int kb0 = (int)(((long)KB * z) / S), kb1 = (int)(((long)KB * (z + 1)) / S);
-    const int NKB = kb1 - kb0;
     const size_t BNrows = (size_t)p.B * p.N;
     const int row = warp * 32 + lane;         // epilogue row (warps 0–3)
     float *lg = reinterpret_cast<float *>(base) + (size_t)(row & (BM - 1)) * LS;
@@ -441,6 +552,29 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
                 cp_async_arrive_noinc(full0 + 8 * s);
             }
             cp_async_wait<0>();
+        } else if (warp == 0) {
+            // ---- sparse tile: one thread gathers the valid rows (4-row groups) per stage with
+            // TMA gather4, while warp 5 streams W_g (two issuers, one stage barrier)
+            if (lane == 0) {
+                const int ng = (nrow + 3) >> 2;
+                const int lrow = l * (int)BNrows;
+                for (int i = 0; i < NKB; i++) {
+                    const int kb = kb0 + i, s = i % STAGES;
+                    if (i >= STAGES) mbar_wait(empty0 + 8 * s, ((i / STAGES) - 1) & 1);
+                    mbar_expect_tx(full0 + 8 * s, 512u * ng);
+                    for (int g4 = 0; g4 < ng; g4++) {
+                        int rr[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const int row_ = 4 * g4 + u;
+                            rr[u] = lrow + ridx[row_ < nrow ? row_ : 0];
+                        }
+                        tma_gather4(A(s) + g4 * 512, &hmap, full0 + 8 * s, kb * BK, rr[0], rr[1], rr[2], rr[3]);
+                    }
+                    mbar_arrive_cnt(full0 + 8 * s, NPROD);
+                }
+            }
+            __syncwarp();
         }
         // ---- stage the (partial) accumulator: TMEM → registers → shared memory
         if (tr0 && threadIdx.x == 0) p.trace[192] = gtimer();
@@ -479,27 +613,16 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
         }
         __syncwarp();
     } else {
-        // ---- operands via TMA: W_g k-block (2D tile) + the tile's hidden rows (gather4,
-        // only the groups holding valid rows; rows past T in the last group repeat a valid
-        // row — an A row only feeds its own D row, which nobody reads)
+        // ---- W_g k-blocks via TMA (3D box, the first `first` were issued in the prologue); the
+        // hidden rows come from warps 0–3 (rows past T in a sparse tile's last gather4 group
+        // repeat a valid row — an A row only feeds its own D row, which nobody reads)
         if (lane == 0) {
-            const int ng = sparse ? (nrow + 3) >> 2 : 0;
-            const int lrow = l * (int)BNrows;
-            for (int i = 0; i < NKB; i++) {
+            for (int i = first; i < NKB; i++) {
                 const int kb = kb0 + i, s = i % STAGES;
-                if (i >= STAGES) mbar_wait(empty0 + 8 * s, ((i / STAGES) - 1) & 1);
+                mbar_wait(empty0 + 8 * s, ((i / STAGES) - 1) & 1);
                 if (tr0 && i < 64) p.trace[64 + i] = gtimer();
-                mbar_arrive_tx(full0 + 8 * s, B_BYTES + 512u * ng);
+                mbar_arrive_tx(full0 + 8 * s, B_BYTES);
                 tma_load_3d(Bs(s), &wmap, full0 + 8 * s, kb * BK, 0, l);
-                for (int g4 = 0; g4 < ng; g4++) {
-                    int rr[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const int row_ = 4 * g4 + u;
-                        rr[u] = lrow + ridx[row_ < nrow ? row_ : 0];
-                    }
-                    tma_gather4(A(s) + g4 * 512, &hmap, full0 + 8 * s, kb * BK, rr[0], rr[1], rr[2], rr[3]);
-                }
             }
         }
         __syncwarp();
@@ -556,7 +679,8 @@ k_router(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUten
                 const int rg = m0 + rr;
                 int32_t *o = p.topk_ids ? p.topk_ids + ((size_t)l * BNrows + rg) * p.K : nullptr;
                 const float *lrow = reinterpret_cast<const float *>(base) + (size_t)rr * LS;
-                const Bits<NE> wr = topk_warp_row<NE>(lrow, p.K, o, lane);
+                const Bits<NE> wr = p.K <= 8 ? topk_warp_merge<NE, 8>(lrow, p.K, o, lane)
+                                             : topk_warp_merge<NE, 16>(lrow, p.K, o, lane);
                 if (lane == 0) {
                     unsigned long long *dst = p.bits + ((size_t)(ridx[rr] / p.N) * p.L + l) * p.EWo;
 #pragma unroll
@@ -729,53 +853,67 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
                                                                                           : (size_t)B * N;
     const int tiles = (int)((rows_bound + BM - 1) / BM);
     const int KB = d / BK;
-    int S = evict::dev_sms() / (tiles * L);
-    S = S < 1 ? 1 : (S > 4 ? 4 : S);
-    if (S > KB) S = KB;
-    // clusters are placed GPC by GPC: take the largest S whose tiles·L clusters are all
-    // co-resident (a second wave would double the time)
-    // (per device: the query answers for the current device)
-    static int max_clusters[kMaxDev][5] = {};
-    static bool mc_known[kMaxDev][5] = {};
+    // Split the d-reduction over a cluster of S CTAs when the (tile, layer) grid would leave SMs
+    // idle (batch-1 serving: one 128-row tile × L layers < #SMs).  Every CTA streams its W_g
+    // k-blocks as 128-byte rows, so the per-SM request rate, not HBM, bounds a lone CTA: the more
+    // SMs stream, the closer the call gets to the HBM roofline.  Candidates: the 6-stage ring
+    // (1 CTA/SM, S ≤ SMs/(tiles·L)) and the 3-stage ring (2 CTAs/SM, S ≤ 2·SMs/(tiles·L));
+    // clusters are placed GPC by GPC, so a split counts only if all tiles·L clusters are
+    // co-resident (cudaOccupancyMaxActiveClusters; a second wave would double the time).
+    const int sms = evict::dev_sms();
+    const long grid1 = (long)tiles * L;
+    static int max_clusters[kMaxDev][2][5] = {};
+    static bool mc_known[kMaxDev][2][5] = {};
     static std::mutex mc_mu;
-    while (S > 1 && !wide) {   // 256 experts: 1 CTA/SM and ≤ 4-CTA clusters — placed without the query
-        int mc;
-        {
-            std::lock_guard<std::mutex> g(mc_mu);
-            if (!mc_known[dev][S]) {
-                cudaLaunchConfig_t q = {};
-                q.gridDim = dim3((unsigned)S, 1u, 1u);
-                q.blockDim = dim3(THREADS, 1, 1);
-                q.dynamicSmemBytes = wide ? smem_bytes<256>(4) : smem_bytes<128>(6);
-                cudaLaunchAttribute a[1];
-                a[0].id = cudaLaunchAttributeClusterDimension;
-                a[0].val.clusterDim.x = (unsigned)S;
-                a[0].val.clusterDim.y = 1;
-                a[0].val.clusterDim.z = 1;
-                q.attrs = a;
-                q.numAttrs = 1;
-                int n = 0;
-                const cudaError_t qe = wide ? cudaOccupancyMaxActiveClusters(&n, k_router<256, 4>, &q)
-                                            : cudaOccupancyMaxActiveClusters(&n, k_router<128, 6>, &q);
-                max_clusters[dev][S] = qe == cudaSuccess ? n : 0;
-                mc_known[dev][S] = true;
-            }
-            mc = max_clusters[dev][S];
+    auto fits = [&](int deep, int S_) -> bool {   // deep: 6-stage (1 CTA/SM), else 3-stage
+        std::lock_guard<std::mutex> g(mc_mu);
+        if (!mc_known[dev][deep][S_]) {
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3((unsigned)S_, 1u, 1u);
+            q.blockDim = dim3(THREADS, 1, 1);
+            q.dynamicSmemBytes = deep ? smem_bytes<128>(6) : smem_bytes<128>(3);
+            cudaLaunchAttribute a[1];
+            a[0].id = cudaLaunchAttributeClusterDimension;
+            a[0].val.clusterDim.x = (unsigned)S_;
+            a[0].val.clusterDim.y = 1;
+            a[0].val.clusterDim.z = 1;
+            q.attrs = a;
+            q.numAttrs = 1;
+            int n = 0;
+            const cudaError_t qe = deep ? cudaOccupancyMaxActiveClusters(&n, k_router<128, 6>, &q)
+                                        : cudaOccupancyMaxActiveClusters(&n, k_router<128, 3>, &q);
+            max_clusters[dev][deep][S_] = qe == cudaSuccess ? n : 0;
+            mc_known[dev][deep][S_] = true;
         }
-        if (mc >= tiles * L) break;
-        S--;
+        return max_clusters[dev][deep][S_] >= grid1;
+    };
+    int S = 1, deep = grid1 <= sms;
+    if (wide) {
+        // 256 experts: 48 KB stages, 1 CTA/SM, ≤ 4-CTA clusters — placed without the query
+        S = (int)(sms / grid1);
+        S = S < 1 ? 1 : (S > 4 ? 4 : S);
+    } else {
+        for (int S_ = 4; S_ >= 2 && S == 1; S_--) {
+            if (S_ > KB) continue;
+            if ((long)S_ * grid1 <= sms && fits(1, S_)) { S = S_; deep = 1; }
+            else if ((long)S_ * grid1 <= 2L * sms && fits(0, S_)) { S = S_; deep = 0; }
+        }
+    }
+    if (const char *ov = getenv("EVICT_ROUTER_SPLITS")) {   // measurement override (dev only)
+        const int o = atoi(ov);
+        if (o >= 1 && o <= 4 && o <= KB) { S = o; if (!wide) deep = (long)S * grid1 <= sms; }
     }
     p.splits = S;
     if (S == 1) {
         dim3 grid((unsigned)tiles, (unsigned)L, 1u);
         if (wide) k_router<256, 4><<<grid, THREADS, smem_bytes<256>(4), s>>>(map, hmap, p);
-        else if ((long)tiles * L > evict::dev_sms()) k_router<128, 3><<<grid, THREADS, smem_bytes<128>(3), s>>>(map, hmap, p);
+        else if (!deep) k_router<128, 3><<<grid, THREADS, smem_bytes<128>(3), s>>>(map, hmap, p);
         else k_router<128, 6><<<grid, THREADS, smem_bytes<128>(6), s>>>(map, hmap, p);
     } else {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)tiles, (unsigned)L, (unsigned)S);
         cfg.blockDim = dim3(THREADS, 1, 1);
-        cfg.dynamicSmemBytes = wide ? smem_bytes<256>(4) : smem_bytes<128>(6);
+        cfg.dynamicSmemBytes = wide ? smem_bytes<256>(4) : (deep ? smem_bytes<128>(6) : smem_bytes<128>(3));
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -785,7 +923,8 @@ static evict_status_t router_impl(const evict_trees_t *trees, const int32_t *ver
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         const cudaError_t le = wide ? cudaLaunchKernelEx(&cfg, k_router<256, 4>, map, hmap, p)
-                                    : cudaLaunchKernelEx(&cfg, k_router<128, 6>, map, hmap, p);
+                               : deep ? cudaLaunchKernelEx(&cfg, k_router<128, 6>, map, hmap, p)
+                                      : cudaLaunchKernelEx(&cfg, k_router<128, 3>, map, hmap, p);
         if (le != cudaSuccess) return EVICT_ERR_CUDA;
     }
     if (cudaGetLastError() != cudaSuccess) return EVICT_ERR_CUDA;
