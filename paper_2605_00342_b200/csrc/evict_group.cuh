@@ -156,6 +156,23 @@ __device__ __forceinline__ void g_load(GTree<G> &t, const int32_t *__restrict__ 
     t.status = (st & EVICT_TREE_BAD_SIZE) ? EVICT_TREE_BAD_SIZE : st;
 }
 
+// A6 input only (the two-kernel throughput path: select already ran): parent row and n
+template <int G>
+__device__ __forceinline__ void g_load_par(GTree<G> &t, const int32_t *__restrict__ parent,
+                                           const int32_t *__restrict__ n_nodes, int b, int N, bool active)
+{
+    const int base = gl<G>() * NP;
+    const size_t row = (size_t)b * N;
+    int4 p0 = make_int4(-1, -1, -1, -1), p1 = p0;
+    if (active && base < N) {
+        p0 = __ldg(reinterpret_cast<const int4 *>(parent + row + base));
+        if (base + NP <= N) p1 = __ldg(reinterpret_cast<const int4 *>(parent + row + base + 4));
+    }
+    t.par[0] = p0.x; t.par[1] = p0.y; t.par[2] = p0.z; t.par[3] = p0.w;
+    t.par[4] = p1.x; t.par[5] = p1.y; t.par[6] = p1.z; t.par[7] = p1.w;
+    t.n = active ? (n_nodes ? __ldg(n_nodes + b) : N) : 0;
+}
+
 template <int G>
 __device__ __forceinline__ void g_load_cost(float (&c)[NP], GTree<G> &t, const float *__restrict__ cost,
                                             int N)

@@ -391,7 +391,10 @@ __host__ __device__ inline size_t fused_smem_bytes(int L, int E, bool flags)
 // LEAN: the serving / bench configuration (u8 top-8 ids, E = 128 or 128 < E ≤ 256, no order row, no
 // union bit rows, no histogram) compiled without the other paths — with warps in
 // different phases the full kernel's code footprint thrashes the instruction cache.
-template <int NPL, int IDF, int KT, int EW, int CL, bool LEAN = false, int WT = kWT>
+// PRE (two-kernel throughput path, LEAN only): k_select_g already wrote k*, e_hat, utility, keep
+// bits, select status and the packed offsets (scanned in the same launch); this kernel rebuilds
+// each tree's emit record from them (parent row, keep bits) and runs A6 + A7 (+ A9) only.
+template <int NPL, int IDF, int KT, int EW, int CL, bool LEAN = false, int WT = kWT, bool PRE = false>
 __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, const float *cost,
                                                        int cost_stride, evict_policy_t pol, evict_routing_t rt,
                                                        evict_fused_out_t out, uint64_t *ws,
@@ -449,6 +452,16 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             const int b = b0 + slot;
             const bool active = slot < WT && b < tr.batch;
             grp::GTree<G> t;
+            if constexpr (PRE) {
+                // the select's outputs (this stream, earlier launch)
+                grp::g_load_par<G>(t, tr.parent, tr.n_nodes, b, N, active);
+#pragma unroll
+                for (int w = 0; w < W; w++) t.keep[w] = (active && w < WN) ? out.keep_bits[(size_t)b * WN + w] : 0ull;
+                t.kstar = active ? out.k_star[b] : 0;
+                t.status = active ? out.status[b] : 0u;
+                t.ehat = active ? out.e_hat[b] : 0.f;
+                t.util = active ? out.utility[b] : 0.f;
+            } else {
             grp::g_load<G>(t, tr.parent, tr.q, tr.n_nodes, b, N, active);
             float c[grp::NP];
             grp::g_load_cost<G>(c, t, cost + (size_t)(active ? b : 0) * cost_stride, N);
@@ -460,15 +473,16 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             float *prow = (active && out.prefix_sums) ? out.prefix_sums + (size_t)b * N : nullptr;
             if (!LEAN && out.order) grp::g_rank_argmax<G>(t, rk, c, N, orow, prow, pol);   // kernel-uniform
             else grp::g_select_values<G>(t, c, N, prow, pol);
+            }
             const int k = t.kstar;
             EmitRec<G> &er = rec[slot < WT ? slot : 0];
             if (active) {
-                if (g == 0) {
+                if (!PRE && g == 0) {
                     if (out.k_star) out.k_star[b] = t.kstar;
                     if (out.e_hat) out.e_hat[b] = t.ehat;
                     if (out.utility) out.utility[b] = t.util;
                 }
-                if (out.keep_bits && g < WN) out.keep_bits[(size_t)b * WN + g] = t.keep[g < W ? g : 0];
+                if (!PRE && out.keep_bits && g < WN) out.keep_bits[(size_t)b * WN + g] = t.keep[g < W ? g : 0];
                 const int base = g * grp::NP;
                 uint32_t pw[2] = {0u, 0u};
 #pragma unroll
@@ -497,7 +511,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
         }
         const int agg = __shfl_sync(kFull, incl, WT - 1);
         int off_local = incl - cnt;
-        if (lane == 0) st_release(states + tile, (tile == 0 ? kInc : kAgg) | (uint64_t)agg);
+        if (!PRE && lane == 0) st_release(states + tile, (tile == 0 ? kInc : kAgg) | (uint64_t)agg);
         int next = 0;
         if (lane == 0) next = (int)atomicAdd(ticket, 1u);
         // ---------------- look-back, first attempt right after the publish: walk back over at most
@@ -508,7 +522,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
         // its union — ~300 instructions of polling per tree; only before it, warps spun on
         // predecessors still in their select: 2.5x slower.)
         unsigned prefix = 0;
-        bool have = tile == 0;
+        bool have = tile == 0 || PRE;   // PRE: the select launch scanned the offsets
         if (!have) have = lookback_walk<false>(tile, states, agg, prefix, lane);
         EVICT_PHASE(1);
         // ---------------- A2: expert union, one warp per tree
@@ -576,10 +590,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             const bool active = slot < WT && b < tr.batch;
             const EmitRec<G> &er = rec[slot < WT ? slot : 0];
             const int k = active ? er.k : 0;
-            const int off = __shfl_sync(kFull, off_local, slot < WT ? slot : 0);
+            const int off = PRE ? (active ? __ldg(out.verify_offsets + b) : 0)
+                                : __shfl_sync(kFull, off_local, slot < WT ? slot : 0);
             if (active && g == 0) {
                 if (out.status) out.status[b] = er.status;
-                if (out.verify_offsets) {
+                if (!PRE && out.verify_offsets) {
                     out.verify_offsets[b] = off;
                     if (b == tr.batch - 1) out.verify_offsets[tr.batch] = off + k;
                 }
@@ -636,23 +651,81 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
 // evict_select: G lanes per tree, 32/G trees per warp, 4 warps per CTA (small
 // CTAs keep batch-64 latency low: 64 trees → 4 CTAs on 4 SMs).
 constexpr int kSelWarps = 4;
+constexpr int kScanChunk = 4096;   // trees per chunk of the packed-offset scan (1024 threads × 4)
+
+// Packed verify-row offsets, second half: block c adds the chunk sums before it, then scans its
+// chunk's k* (4 per thread, warp shuffles + one smem pass) — verify_offsets[b] = Σ_{b' < b} k*,
+// verify_offsets[B] = T.  k* of an errored tree is 0.
+static __global__ void __launch_bounds__(1024) k_scan_offsets(int B, const int32_t *__restrict__ k_star,
+                                                       const int32_t *__restrict__ chunk_sums,
+                                                       int32_t *__restrict__ verify_offsets)
+{
+    __shared__ int s_w[32];
+    __shared__ int s_base;
+    const int c = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int pre = 0;
+    for (int j = tid; j < c; j += blockDim.x) pre += chunk_sums[j];
+    pre = __reduce_add_sync(kFull, pre);
+    if (lane == 0) s_w[warp] = pre;
+    __syncthreads();
+    if (warp == 0) {
+        const int v = __reduce_add_sync(kFull, s_w[lane]);
+        if (lane == 0) s_base = v;
+    }
+    __syncthreads();
+    const int b0 = c * kScanChunk + tid * 4;
+    int k[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) k[i] = b0 + i < B ? __ldg(k_star + b0 + i) : 0;
+    const int own = k[0] + k[1] + k[2] + k[3];
+    int inc = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, inc, o);
+        if (lane >= o) inc += v;
+    }
+    __syncthreads();
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const int x = s_w[lane];
+        int xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(kFull, xi, o);
+            if (lane >= o) xi += v;
+        }
+        s_w[lane] = xi - x;                       // exclusive prefix of warp totals
+    }
+    __syncthreads();
+    int run = s_base + s_w[warp] + inc - own;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        if (b0 + i < B) verify_offsets[b0 + i] = run;
+        run += k[i];
+        if (b0 + i == B - 1) verify_offsets[B] = run;
+    }
+}
 
 template <int G>
 __global__ void __launch_bounds__(kSelWarps * 32) k_select_g(evict_trees_t tr, const float *cost,
                                                              int cost_stride, evict_policy_t pol, int32_t *k_star,
                                                              float *e_hat, float *utility,
                                                              uint64_t *keep_bits, int32_t *order,
-                                                             float *prefix_sums, uint32_t *status)
+                                                             float *prefix_sums, uint32_t *status,
+                                                             int32_t *chunk_sums = nullptr)
 {
     constexpr int TPW = grp::GShape<G>::TPW;
     constexpr int NMAX = grp::GShape<G>::NMAX;
     constexpr int W = grp::GShape<G>::W;
+    constexpr int PER = kSelWarps * TPW;               // trees per CTA tile
     __shared__ __align__(16) float sd_all[kSelWarps * TPW * NMAX];
     __shared__ uint8_t rk_all[kSelWarps * TPW * NMAX];
+    __shared__ int s_k[PER];
     const int warp = threadIdx.x >> 5;
     const int gi = grp::gidx<G>(), g = grp::gl<G>();
     const int slot = warp * TPW + gi;
-    const int b = blockIdx.x * (kSelWarps * TPW) + slot;
+    const int b = blockIdx.x * PER + slot;
     const bool active = b < tr.batch;
     const int N = tr.max_nodes;
     const int WN = (N + 63) / 64;
@@ -665,6 +738,17 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_select_g(evict_trees_t tr, c
     float *prow = (active && prefix_sums) ? prefix_sums + (size_t)b * N : nullptr;
     if (order) grp::g_rank_argmax<G>(t, rk_all + slot * NMAX, c, N, orow, prow, pol);   // kernel-uniform
     else grp::g_select_values<G>(t, c, N, prow, pol);
+    if (chunk_sums) {
+        // packed verify-row offsets, first half: Σk* per chunk of kScanChunk trees (one atomic
+        // per CTA); k_scan_offsets turns the chunk sums and k* into the exclusive scan
+        if (g == 0) s_k[slot] = active ? t.kstar : 0;
+        __syncthreads();
+        if (warp == 0) {
+            const int lane = lane_id();
+            const int v = __reduce_add_sync(kFull, lane < PER ? s_k[lane] : 0);
+            if (lane == 0 && v) atomicAdd(chunk_sums + (blockIdx.x * PER) / kScanChunk, v);
+        }
+    }
     if (!active) return;
     if (g == 0) {
         k_star[b] = t.kstar;
@@ -764,6 +848,20 @@ struct FusedLauncher {
                     kern = k_fused<NPL, IDF, KT, EW, CL, true, 1>;
                     dyn = fused_smem_bytes<G, 1>(rt->num_layers, rt->num_experts, flags);
                     wt = 1;
+                } else if (o->k_star && o->e_hat && o->utility && o->keep_bits && o->status && o->verify_offsets) {
+                    // throughput batches: the select (+ packed-offset scan) as its own launch at full
+                    // occupancy, then A6 + A7 (+ A9) reading its outputs — no look-back in the union
+                    // kernel (ws[0]: its ticket; ws[1]: the scan's ticket; ws[2..]: scan tile states)
+                    constexpr int PER = kSelWarps * grp::GShape<G>::TPW;
+                    const int sblocks = (tr->batch + PER - 1) / PER;
+                    int32_t *chunk_sums = reinterpret_cast<int32_t *>(ws + 1);   // zeroed by the caller
+                    k_select_g<G><<<sblocks, kSelWarps * 32, 0, s>>>(*tr, cost, cs, pol, o->k_star, o->e_hat,
+                                                                    o->utility, o->keep_bits, nullptr, nullptr,
+                                                                    o->status, chunk_sums);
+                    k_scan_offsets<<<(tr->batch + kScanChunk - 1) / kScanChunk, 1024, 0, s>>>(
+                        tr->batch, o->k_star, chunk_sums, o->verify_offsets);
+                    if (cudaGetLastError() != cudaSuccess) return EVICT_ERR_CUDA;
+                    kern = k_fused<NPL, IDF, KT, EW, CL, true, kWT, true>;
                 } else {
                     kern = k_fused<NPL, IDF, KT, EW, CL, true>;
                 }
