@@ -173,19 +173,26 @@ __device__ __forceinline__ void g_load_par(GTree<G> &t, const int32_t *__restric
     t.n = active ? (n_nodes ? __ldg(n_nodes + b) : N) : 0;
 }
 
+// cost row: the loads (g_fetch_cost, independent of the tree — issue them before the tree's own
+// loads are consumed) and the validation against n (g_apply_cost)
 template <int G>
-__device__ __forceinline__ void g_load_cost(float (&c)[NP], GTree<G> &t, const float *__restrict__ cost,
-                                            int N)
+__device__ __forceinline__ void g_fetch_cost(float4 (&cr)[2], const float *__restrict__ cost, int N, bool active)
 {
     const int base = gl<G>() * NP;
     // cost rows are 16-byte aligned with N % 4 == 0 (host-checked): two vector loads
-    float4 c0 = make_float4(1.f, 1.f, 1.f, 1.f), c1 = c0;
-    if (!(t.status & EVICT_TREE_BAD_SIZE) && base < t.n) {
-        c0 = __ldg(reinterpret_cast<const float4 *>(cost + base));
-        if (base + 4 < N) c1 = __ldg(reinterpret_cast<const float4 *>(cost + base + 4));
+    cr[0] = make_float4(1.f, 1.f, 1.f, 1.f);
+    cr[1] = cr[0];
+    if (active && base < N) {
+        cr[0] = __ldg(reinterpret_cast<const float4 *>(cost + base));
+        if (base + 4 < N) cr[1] = __ldg(reinterpret_cast<const float4 *>(cost + base + 4));
     }
-    c[0] = c0.x; c[1] = c0.y; c[2] = c0.z; c[3] = c0.w;
-    c[4] = c1.x; c[5] = c1.y; c[6] = c1.z; c[7] = c1.w;
+}
+template <int G>
+__device__ __forceinline__ void g_apply_cost(float (&c)[NP], GTree<G> &t, const float4 (&cr)[2])
+{
+    const int base = gl<G>() * NP;
+    c[0] = cr[0].x; c[1] = cr[0].y; c[2] = cr[0].z; c[3] = cr[0].w;
+    c[4] = cr[1].x; c[5] = cr[1].y; c[6] = cr[1].z; c[7] = cr[1].w;
     uint32_t st = 0;
 #pragma unroll
     for (int r = 0; r < NP; r++) {
@@ -198,6 +205,14 @@ __device__ __forceinline__ void g_load_cost(float (&c)[NP], GTree<G> &t, const f
         }
     }
     t.status |= g_or<G>(st);
+}
+template <int G>
+__device__ __forceinline__ void g_load_cost(float (&c)[NP], GTree<G> &t, const float *__restrict__ cost,
+                                            int N)
+{
+    float4 cr[2];
+    g_fetch_cost<G>(cr, cost, N, !(t.status & EVICT_TREE_BAD_SIZE));
+    g_apply_cost<G>(c, t, cr);
 }
 
 // ------------------------------------------------------------ A2

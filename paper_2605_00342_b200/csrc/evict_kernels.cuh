@@ -462,9 +462,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 t.ehat = active ? out.e_hat[b] : 0.f;
                 t.util = active ? out.utility[b] : 0.f;
             } else {
+            float4 cr[2];
+            grp::g_fetch_cost<G>(cr, cost + (size_t)(active ? b : 0) * cost_stride, N, active);
             grp::g_load<G>(t, tr.parent, tr.q, tr.n_nodes, b, N, active);
             float c[grp::NP];
-            grp::g_load_cost<G>(c, t, cost + (size_t)(active ? b : 0) * cost_stride, N);
+            grp::g_apply_cost<G>(c, t, cr);
             // per-tree score arrays 8 floats apart in bank space: the 4 trees' reads of
             // their roots (and other equal node ids) land on different banks
             float *sd = reinterpret_cast<float *>(wscr) + gi * (NMAX + 8);
@@ -545,9 +547,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 EmitRec<G> &er = rec[slot];
                 uint32_t st = er.status;
                 if constexpr (LEAN && EW == 2) {
-                    tree_union_flags64<1, CL, true, false>(st, er.klist, er.k, b, N, L, E, rt.ids, wscr,
-                                                           out.union_count, out.union_total, nullptr,
-                                                           &epoch, fstats ? lsum : nullptr);
+                    tree_union_flags64<1, CL, true, false, false, WT == 1 ? 8 : 4>(
+                        st, er.klist, er.k, b, N, L, E, rt.ids, wscr, out.union_count, out.union_total, nullptr,
+                        &epoch, fstats ? lsum : nullptr);
                     if constexpr (kFold) {
                         if (fstats && lane == 0) {
                             unsigned *wsc = fs->sc[warp];
@@ -566,9 +568,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                     }
                 }
                 else if constexpr (LEAN)   // 128 < E ≤ 256 (Ling-flash-2.0): 32-byte expert rows
-                    tree_union_flags64<1, CL, false, false, true>(st, er.klist, er.k, b, N, L, E, rt.ids, wscr,
-                                                                  out.union_count, out.union_total, nullptr,
-                                                                  &epoch);
+                    tree_union_flags64<1, CL, false, false, true, WT == 1 ? 8 : 4>(
+                        st, er.klist, er.k, b, N, L, E, rt.ids, wscr, out.union_count, out.union_total, nullptr,
+                        &epoch);
                 else
                     tree_union<NPL, IDF, KT, EW, CL>(st, er.klist, er.k, b, N, L, rt.top_k, E, rt.id_format,
                                                      rt.ids, wscr, Epad, out.union_count, out.union_total,
@@ -730,9 +732,11 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_select_g(evict_trees_t tr, c
     const int N = tr.max_nodes;
     const int WN = (N + 63) / 64;
     grp::GTree<G> t;
+    float4 cr[2];
+    grp::g_fetch_cost<G>(cr, cost + (size_t)(active ? b : 0) * cost_stride, N, active);
     grp::g_load<G>(t, tr.parent, tr.q, tr.n_nodes, b, N, active);
     float c[grp::NP];
-    grp::g_load_cost<G>(c, t, cost + (size_t)(active ? b : 0) * cost_stride, N);
+    grp::g_apply_cost<G>(c, t, cr);
     grp::g_levels<G, true>(t, sd_all + slot * NMAX);
     int32_t *orow = (active && order) ? order + (size_t)b * N : nullptr;
     float *prow = (active && prefix_sums) ? prefix_sums + (size_t)b * N : nullptr;

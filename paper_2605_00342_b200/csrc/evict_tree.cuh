@@ -1117,7 +1117,9 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr)
 // W256 (128 < E ≤ 256, Ling-flash-2.0): the same scheme with 32-byte expert rows — passes
 // of 32 layers, flag(l, e) at byte e·32 + 4·(l%8) + (l/8)%4; the read-back widens the byte
 // sums to 16-bit lanes before the cross-lane reduction (a layer can hold all 256 experts).
-template <int IDF, int R, bool E128, bool BITS, bool W256 = false>
+// UB: nodes per load batch for u8 ids (4 for throughput; 8 in the serving-batch kernel, where one
+// DRAM round trip covers a typical tree's kept rows and registers are not scarce)
+template <int IDF, int R, bool E128, bool BITS, bool W256 = false, int UB = 4>
 __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8_t *__restrict__ klist, int k,
                                                    int b, int N, int L, int E, const void *__restrict__ ids,
                                                    uint8_t *flags, int32_t *__restrict__ union_count,
@@ -1140,7 +1142,7 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
     const int ep = mark ? *epoch : 0;
     const uint32_t marker = 1u << ep;
     constexpr int RP = R < RPP ? R : RPP;              // rounds per pass
-    constexpr int U = IDF == 1 ? 4 : 1;                // nodes per load batch (i32 rows are 4x wider)
+    constexpr int U = IDF == 1 ? UB : 1;               // nodes per load batch (i32 rows are 4x wider)
     const int lane = lane_id();
     const int S = 2 * L;
     const uint32_t row = (uint32_t)S;                  // 4-id units per node row
