@@ -227,7 +227,8 @@ evict_status_t evict_select_build_union_policy(const evict_trees_t *trees, const
     // folded into the launch for the single-pass E = 128 serving union (k_fused kFold), else the
     // statistics kernel runs after it
     const int L = out->union_count ? rt->num_layers : 0;
-    const bool fold = want_stats && out->union_count && rt->id_format == EVICT_ID_U8 && rt->top_k == 8 &&
+    const bool fold = want_stats && trees->batch > kFusedSmallBatch && out->union_count &&
+                      rt->id_format == EVICT_ID_U8 && rt->top_k == 8 &&
                       rt->num_experts == 128 && L <= 64 && !out->order && !out->union_bits && !out->expert_hist;
     evict_fused_out_t o = *out;
     if (want_stats) {

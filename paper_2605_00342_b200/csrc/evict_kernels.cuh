@@ -833,6 +833,78 @@ struct UnionLauncher {
     }
 };
 
+// ------------------------------------------------------------ fused, serving batches
+// Batches up to kSmallBatch in the u8 serving configuration: one warp per tree, the latency
+// chain of k_select (32 lanes × NPL nodes: the shortest select) → publish k* → expert union
+// (8 kept rows per load batch: one DRAM round trip for a typical tree) → decoupled look-back for
+// the packed offset → warp-wide emit (k_build's tree_build_emit).  Tree b is warp b of the grid
+// (every warp is resident for B ≤ kSmallBatch), so predecessors always run.  ws[1 + b]: tile
+// states.  Statistics are not folded here (the call runs k_stats when they are requested).
+template <int NPL, int EW, int CL, int WPC>   // WPC: warps (trees) per CTA
+__global__ void __launch_bounds__(WPC * 32) k_fused_lat(evict_trees_t tr, const float *cost, int cost_stride,
+                                                         evict_policy_t pol, evict_routing_t rt,
+                                                         evict_fused_out_t out, uint64_t *ws)
+{
+    constexpr int W = Shape<NPL>::W;
+    extern __shared__ __align__(16) uint8_t dsm[];       // WPC × 8 KB union flag blocks
+    __shared__ WarpSlab<NPL> slab[WPC];
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    const int b = blockIdx.x * WPC + warp;
+    if (b >= tr.batch) return;
+    uint8_t *flags = dsm + (size_t)warp * 8192;
+    uint4 *f4 = reinterpret_cast<uint4 *>(flags);
+    for (int i = lane; i < 8192 / 16; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
+    const int N = tr.max_nodes;
+    const int WN = (N + 63) / 64;
+    const int L = rt.num_layers, E = rt.num_experts;
+    WarpSlab<NPL> &sm = slab[warp];
+    TreeState<NPL> t;
+    tree_load_validate<NPL>(t, tr, tr.parent, tr.q, tr.n_nodes, b, N);
+    float c[NPL];
+    if (!(t.status & EVICT_TREE_BAD_SIZE)) tree_load_cost<NPL>(c, t, cost + (size_t)b * cost_stride);
+    if (!t.status) {
+        tree_levels<NPL, true>(t, sm);
+        tree_rank_argmax<NPL>(t, sm, c, N, nullptr, nullptr, pol);
+    } else {
+        t.kstar = 0; t.ehat = 0.f; t.util = 0.f;
+#pragma unroll
+        for (int w = 0; w < W; w++) t.keep[w] = 0ull;
+    }
+    const int k = t.kstar;
+    uint64_t *states = ws + 1;
+    if (lane == 0) {
+        st_release(states + b, (b == 0 ? kInc : kAgg) | (uint64_t)k);
+        if (out.k_star) out.k_star[b] = t.kstar;
+        if (out.e_hat) out.e_hat[b] = t.ehat;
+        if (out.utility) out.utility[b] = t.util;
+    }
+    if (out.keep_bits && lane < WN) out.keep_bits[(size_t)b * WN + lane] = t.keep[lane < W ? lane : 0];
+    if (!t.status) tree_fill_klist<NPL>(t, sm);
+    uint32_t st = t.status;
+    int epoch = 0;
+    __syncwarp();
+    if constexpr (EW == 2)
+        tree_union_flags64<1, CL, true, false, false, 8>(st, sm.klist, k, b, N, L, E, rt.ids, flags,
+                                                         out.union_count, out.union_total, nullptr, &epoch);
+    else
+        tree_union_flags64<1, CL, false, false, true, 8>(st, sm.klist, k, b, N, L, E, rt.ids, flags,
+                                                         out.union_count, out.union_total, nullptr, &epoch);
+    unsigned prefix = 0;
+    if (b > 0) lookback_walk<true>(b, states, k, prefix, lane);
+    const int off = (int)prefix;
+    if (lane == 0) {
+        if (out.status) out.status[b] = st;
+        if (out.verify_offsets) {
+            out.verify_offsets[b] = off;
+            if (b == tr.batch - 1) out.verify_offsets[tr.batch] = off + k;
+        }
+    }
+    if (k > 0)
+        tree_build_emit<NPL>(t, sm, k, b, N, off, out.pos_offset ? __ldg(out.pos_offset + b) : 0,
+                             out.kept_index, out.retrieve_index, out.positions, out.next_token,
+                             out.next_sibling, out.tree_mask);
+}
+
 template <int NPL, int IDF, int KT, int EW, int CL>
 struct FusedLauncher {
     // the caller cleared 1 + batch tile states when batch ≤ kSmallBatch (else 1 + ⌈batch/4⌉)
@@ -849,9 +921,16 @@ struct FusedLauncher {
             const bool shape = EW == 2 ? rt->num_experts == 128 : rt->num_experts > 128;
             if (shape && !o->order && !o->union_bits && !o->expert_hist && o->union_count) {
                 if (tr->batch <= kSmallBatch) {
-                    kern = k_fused<NPL, IDF, KT, EW, CL, true, 1>;
-                    dyn = fused_smem_bytes<G, 1>(rt->num_layers, rt->num_experts, flags);
-                    wt = 1;
+                    // up to one SM per tree: a CTA per tree while the batch fits the SMs, else 8 per CTA
+                    if (tr->batch <= dev_sms()) {
+                        k_fused_lat<NPL, EW, CL, 1><<<tr->batch, 32, 8192, s>>>(*tr, cost, cs, pol, *rt, *o, ws);
+                    } else {
+                        auto lk = k_fused_lat<NPL, EW, CL, kWarps>;
+                        const int ldyn = kWarps * 8192;
+                        cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, ldyn);
+                        lk<<<(tr->batch + kWarps - 1) / kWarps, kWarps * 32, ldyn, s>>>(*tr, cost, cs, pol, *rt, *o, ws);
+                    }
+                    return launched();
                 } else if (o->k_star && o->e_hat && o->utility && o->keep_bits && o->status && o->verify_offsets) {
                     // throughput batches: the select (+ packed-offset scan) as its own launch at full
                     // occupancy, then A6 + A7 (+ A9) reading its outputs — no look-back in the union
