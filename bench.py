@@ -715,9 +715,11 @@ def router_bench(ev, gen, torch, stream):
         with torch.cuda.stream(gs):
             for a, c in evs:
                 flush.fill_(1)
+                torch.cuda.nvtx.range_push(f"evict.router.{name}")
                 a.record(gs)
                 graph.replay()
                 c.record(gs)
+                torch.cuda.nvtx.range_pop()
         gs.synchronize()
         us = float(np.median([a.elapsed_time(c) for a, c in evs])) * 1e3
         del flush
@@ -759,12 +761,17 @@ def timed_sweep(args, ev, torch, dist, dev, stream, P, Q, n, cost, ids, M, world
     stats_t, dstats_t = bufs["stats"], bufs["dstats"]
 
     def step(ev0=None, ev1=None):
+        # NVTX ranges: the fused A1–A7 (+ A9) call and the statistics all-reduce, for nsys
+        torch.cuda.nvtx.range_push("evict.fused_step")
         if ev0 is not None:
             ev0.record(stream)
         call(stream)
         if ev1 is not None:
             ev1.record(stream)
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.nvtx.range_push("evict.stats_allreduce")
         allreduce_stats(stats_t, dstats_t)
+        torch.cuda.nvtx.range_pop()
 
     for _ in range(max(3, W)):
         step()
@@ -843,11 +850,14 @@ def run_native(args, rank, world, local_rank):
         "config": config_dict(args, world, M, total),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "k_fused (select+build+union, A9 stats folded in)", "peak_kind": peak_kind,
+                     "kernel": ("evict_select_build_union: k_select_g (A1-A5 + chunk sums) -> k_scan_offsets -> "
+                                "k_fused PRE (A6 + A7 + folded A9); one call = the whole path"
+                                if M > 2048 and args.id_format == "u8" else "k_fused (A1-A7 + A9)"),
+                     "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": abytes, "bytes_split": parts,
                      "kernel_ms": kern_ms},
         "union_hbm_gbs": parts["union"] / (kern_ms / 1e3) / 1e9,
-        "gpu_launches": K,
+        "gpu_launches": (3 if M > 2048 and args.id_format == "u8" else 1) * K,
         "k_star_mean": float(lst[1]) / max(1, M - int(lst[4])),
         "union_mean_per_layer": float(lst[3]) / max(1, (M - int(lst[4])) * L_LAYERS),
         "stats_allreduced_trees": int(st[0]),

@@ -22,10 +22,18 @@ if which in ("all", "fused"):
     ev.evict_union_curve(s["order"], cu(ids), E, n_nodes=cu(n), per_layer=True)
     b = ev.evict_build_verify_tree(cu(P), s["keep_bits"], n_nodes=cu(n))
     ev.evict_expert_union(s["keep_bits"], cu(ids), E, n_nodes=cu(n))
+if which in ("all", "fusedbig"):
+    # the throughput path (select launch + offset scan + union/emit, folded A9) and pinned host ids
+    Bb = 2600
+    Pb, Qb, nb = gen.trees(3, Bb, N, 6, 10)
+    idsb = gen.routing(3, Bb, N, L, E, K)
+    ev.evict_select_build_union(cu(Pb), cu(Qb), cost, cu(idsb), E, n_nodes=cu(nb), with_stats=True)
+    ev.evict_select_build_union(cu(Pb), cu(Qb), cost, torch.from_numpy(idsb).pin_memory(), E, n_nodes=cu(nb))
+    ev.evict_select_build_union(cu(P), cu(Q), cost, cu(ids), E, n_nodes=cu(n), with_stats=True)
 if which in ("all", "router"):
     s = ev.evict_select(cu(P), cu(Q), cost, n_nodes=cu(n))
     b = ev.evict_build_verify_tree(cu(P), s["keep_bits"], n_nodes=cu(n))
-    for Ex in (128, 256):
+    for Ex in (8, 100, 128, 200, 256):
         h = gen.hidden_cuda(3, B, N, 4, 256, mode=1)
         w = gen.wgate_cuda(4, 4, Ex, 256, mode=1)
         ev.evict_router_union(b["verify_offsets"], b["retrieve_index"], h, w, 8, B, N)
