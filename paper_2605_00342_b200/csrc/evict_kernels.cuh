@@ -19,6 +19,7 @@
 #include "evict.h"
 #include "evict_tree.cuh"
 #include "evict_group.cuh"
+#include "evict_launch.h"
 
 namespace evict {
 
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     // only for that configuration; it runs evict_batch_stats after the launch otherwise)
     constexpr bool kFold = LEAN && EW == 2 && CL <= 4;
     const bool fstats = kFold && out.stats != nullptr;
-    uint32_t lsum[2] = {0u, 0u};
+    uint32_t lsum[4] = {0u, 0u, 0u, 0u};   // folded A9: this lane's layers ucols_layer(lane, m)
     if constexpr (kFold) {
         if (fstats) {
             uint32_t *z = reinterpret_cast<uint32_t *>(fs);
@@ -546,10 +547,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 if (b >= tr.batch) break;
                 EmitRec<G> &er = rec[slot];
                 uint32_t st = er.status;
-                if constexpr (LEAN && EW == 2) {
-                    tree_union_flags64<1, CL, true, false, false, WT == 1 ? 8 : 4>(
-                        st, er.klist, er.k, b, N, L, E, rt.ids, wscr, out.union_count, out.union_total, nullptr,
-                        &epoch, fstats ? lsum : nullptr);
+                if constexpr (LEAN && EW == 2 && CL <= 4) {
+                    // lane-owned flag columns (conflict-free byte stores); CL = 3: L ≤ 48, CL = 4: L ≤ 64
+                    tree_union_cols<CL == 4 ? 2 : 1, WT == 1 ? 8 : 4>(st, er.klist, er.k, b, N, L, rt.ids, wscr,
+                                                                   out.union_count, out.union_total, &epoch,
+                                                                   fstats ? lsum : nullptr);
                     if constexpr (kFold) {
                         if (fstats && lane == 0) {
                             unsigned *wsc = fs->sc[warp];
@@ -567,6 +569,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                         }
                     }
                 }
+                else if constexpr (LEAN && EW == 2)
+                    tree_union_flags64<1, CL, true, false, false, WT == 1 ? 8 : 4>(
+                        st, er.klist, er.k, b, N, L, E, rt.ids, wscr, out.union_count, out.union_total, nullptr,
+                        &epoch, nullptr);
                 else if constexpr (LEAN)   // 128 < E ≤ 256 (Ling-flash-2.0): 32-byte expert rows
                     tree_union_flags64<1, CL, false, false, true, WT == 1 ? 8 : 4>(
                         st, er.klist, er.k, b, N, L, E, rt.ids, wscr, out.union_count, out.union_total, nullptr,
@@ -616,12 +622,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     }
     if constexpr (kFold) {
         if (fstats) {
-            // per-lane layer sums (layers 16·(bsel + 2hb) + 4q + m, as in tree_union_flags64)
-            const int q = lane & 3, m = (lane >> 2) & 3, bsel = lane >> 4;
+            // per-lane layer sums (tree_union_cols' output layers)
 #pragma unroll
-            for (int hb = 0; hb < 2; hb++) {
-                const int l = 16 * (bsel + 2 * hb) + 4 * q + m;
-                if (l < L && lsum[hb]) atomicAdd(&fs->lay[l], lsum[hb]);
+            for (int m = 0; m < 4; m++) {
+                const int l = ucols_layer<CL == 4 ? 2 : 1>(lane, m);
+                if (l < L && lsum[m]) atomicAdd(&fs->lay[l], lsum[m]);
             }
             __syncthreads();
             unsigned long long *gs = reinterpret_cast<unsigned long long *>(out.stats);
@@ -944,6 +949,12 @@ struct FusedLauncher {
                     k_scan_offsets<<<(tr->batch + kScanChunk - 1) / kScanChunk, 1024, 0, s>>>(
                         tr->batch, o->k_star, chunk_sums, o->verify_offsets);
                     if (cudaGetLastError() != cudaSuccess) return EVICT_ERR_CUDA;
+#ifdef EVICT_UE
+                    if constexpr (NPL == 2 && EW == 2) {
+                        // A6 + A7 (+ A9): warp per tree, lane-owned flag columns (union_emit.cu)
+                        if (rt->num_layers <= 64) return launch_union_emit(tr, rt, o, s);
+                    }
+#endif
                     kern = k_fused<NPL, IDF, KT, EW, CL, true, kWT, true>;
                 } else {
                     kern = k_fused<NPL, IDF, KT, EW, CL, true>;

@@ -1345,6 +1345,171 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
     if (union_total && lane == 0) union_total[b] = tot;
 }
 
+// Top-8 u8 ids, E = 128, L ≤ 64 (the serving / C5 configuration; Eq. 5) with
+// lane-owned flag columns: lane c owns byte column c of an 8 KB block of 32 rows × 256 B; row
+// r = e >> 2 holds, at byte 4c + (e & 3), the flag of expert e for lane c's layer in region 0
+// (bytes 0–127: layer c, all 8 ids of it from one 8-byte load) and region 1 (bytes 128–255:
+// MODE 1 (32 < L ≤ 48) the half c & 1 of layer 32 + c/2, MODE 2 (48 < L ≤ 64) layer 32 + c).
+// Every byte store of a warp instruction lands on bank c: conflict-free whatever the ids (the
+// slot layout of tree_union_flags64 puts the two halves of a layer on one bank group, ≈ 2
+// wavefronts per store).  The store offset of id e is one PRMT of two per-word vectors:
+// lo = (w & 0x03030303) | column base, hi = (w >> 2) & 0x1F1F1F1F give (e >> 2) << 8 | lo.
+// Marker epochs as in tree_union_flags64 (tree t stores 1 << (t mod 4), the block is cleared
+// after every 4th read-back).  Read-back: lane (q = lane & 7, r0 = lane >> 3) loads rows r0 + 4j
+// (j < 8) as 16-byte vectors (8 lanes per 128-byte phase: conflict-free), sums marker bits
+// bytewise per column, two xor-shuffles over r0, one IDP4A per layer.  Lane outputs: layers
+// ue_lanes_layer(lane, m) (lanes 0–7 region 0, lanes 8–15 region 1; 64 = none).
+template <int MODE>
+__device__ __forceinline__ int ucols_layer(int lane, int m)
+{
+    const int q = lane & 7, r0 = lane >> 3;
+    if (r0 == 0) return 4 * q + m;
+    if (r0 == 1) {
+        if constexpr (MODE == 1) return m < 2 ? 32 + 2 * q + m : 64;
+        if constexpr (MODE == 2) return 32 + 4 * q + m;
+    }
+    return 64;
+}
+__device__ __forceinline__ uint32_t prmt_b32(uint32_t a, uint32_t b, uint32_t sel)
+{
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+__device__ __forceinline__ void ucols_store4(uint32_t fb, uint32_t w, uint32_t cb, uint32_t marker)
+{
+    const uint32_t lo = (w & 0x03030303u) | cb;
+    const uint32_t hi = (w >> 2) & 0x1F1F1F1Fu;
+    // id j: byte 0 = lo.b_j, byte 1 = hi.b_j, bytes 2–3 = sign of hi.b_j (0)
+    sts_u8(fb + prmt_b32(lo, hi, 0xCC40u), marker);
+    sts_u8(fb + prmt_b32(lo, hi, 0xDD51u), marker);
+    sts_u8(fb + prmt_b32(lo, hi, 0xEE62u), marker);
+    sts_u8(fb + prmt_b32(lo, hi, 0xFF73u), marker);
+}
+template <int MODE, int UB>
+__device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t *__restrict__ klist, int k,
+                                                int b, int N, int L, const void *__restrict__ ids,
+                                                uint8_t *flags, int32_t *__restrict__ union_count,
+                                                int32_t *__restrict__ union_total, int *epoch,
+                                                uint32_t *lsum)
+{
+    const int lane = lane_id();
+    const int q = lane & 7, r0 = lane >> 3;
+    const bool run = status == 0 && k > 0;
+    uint32_t cnt[4] = {0u, 0u, 0u, 0u};
+    if (run) {
+        const int ep = *epoch;
+        const uint32_t marker = 1u << ep;
+        const uint32_t fb = (uint32_t)__cvta_generic_to_shared(flags);
+        const uint32_t rowB = (uint32_t)L * 8u;
+        // lanes past the layers re-read byte 0 of the row: their flags land in columns of
+        // layers ≥ L (never counted) and the bytes are ids of the same kept row
+        const bool ld0 = lane < L;
+        const bool ld1 = MODE == 1 ? lane < 2 * (L - 32) : (MODE == 2 ? lane < L - 32 : false);
+        const uint32_t lo0 = ld0 ? 8u * (uint32_t)lane : 0u;
+        const uint32_t lo1 = ld1 ? (MODE == 1 ? 256u + 4u * (uint32_t)lane : 256u + 8u * (uint32_t)lane) : 0u;
+        const uint32_t cb0 = (4u * (uint32_t)lane) * 0x01010101u;
+        const uint32_t cb1 = (128u + 4u * (uint32_t)lane) * 0x01010101u;
+        const uint8_t *tb = reinterpret_cast<const uint8_t *>(ids) + (size_t)b * N * rowB;
+        uint32_t badw = 0u;
+#pragma unroll 1
+        for (int j0 = 0; j0 < k; j0 += UB) {
+            uint2 x0[UB];
+            uint32_t x1[UB], x2[UB];
+#pragma unroll
+            for (int u = 0; u < UB; u++) {
+                const uint8_t *rp = tb + (uint32_t)klist[min(j0 + u, k - 1)] * rowB;
+                x0[u] = __ldg(reinterpret_cast<const uint2 *>(rp + lo0));
+                x1[u] = 0u;
+                x2[u] = 0u;
+                if constexpr (MODE == 1) {
+                    x1[u] = __ldg(reinterpret_cast<const uint32_t *>(rp + lo1));
+                } else if constexpr (MODE == 2) {
+                    const uint2 y = __ldg(reinterpret_cast<const uint2 *>(rp + lo1));
+                    x1[u] = y.x;
+                    x2[u] = y.y;
+                }
+            }
+            // every row of the batch is consumed here, in the loads' own block: the compiler
+            // cannot sink a row's loads behind the previous rows' stores (the store loop's
+            // warp-uniform exits), so one DRAM round trip serves the batch (tail re-reads are
+            // rows k − 1 again: harmless for the id check)
+#pragma unroll
+            for (int u = 0; u < UB; u++) badw |= x0[u].x | x0[u].y | x1[u] | x2[u];
+#pragma unroll
+            for (int u = 0; u < UB; u++) {
+                if (j0 + u >= k) break;   // warp-uniform: a batch's tail re-read stores nothing
+                ucols_store4(fb, x0[u].x, cb0, marker);
+                ucols_store4(fb, x0[u].y, cb0, marker);
+                if constexpr (MODE >= 1) ucols_store4(fb, x1[u], cb1, marker);
+                if constexpr (MODE == 2) ucols_store4(fb, x2[u], cb1, marker);
+            }
+        }
+        __syncwarp();
+        const uint32_t mk = 0x01010101u << ep;
+        const bool clear = ep == 3;
+        uint32_t a0 = 0u, a1 = 0u, a2 = 0u, a3 = 0u, c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint32_t ra = fb + 256u * (uint32_t)(r0 + 4 * j) + 16u * (uint32_t)q;
+            const uint4 x = lds_v4(ra);
+            a0 += x.x & mk; a1 += x.y & mk; a2 += x.z & mk; a3 += x.w & mk;
+            if constexpr (MODE == 1) {
+                const uint4 y = lds_v4(ra + 128u);
+                c0 += (y.x | y.y) & mk;   // layer 32 + 2q (both halves)
+                c1 += (y.z | y.w) & mk;   // layer 33 + 2q
+            } else if constexpr (MODE == 2) {
+                const uint4 y = lds_v4(ra + 128u);
+                c0 += y.x & mk; c1 += y.y & mk; c2 += y.z & mk; c3 += y.w & mk;
+            }
+            if (clear) {
+                sts_v4_zero(ra);
+                if constexpr (MODE >= 1) sts_v4_zero(ra + 128u);
+            }
+        }
+        // ≤ 8 markers per byte after the shift; the sum over the 4 lanes of a column quad ≤ 32
+        a0 >>= ep; a1 >>= ep; a2 >>= ep; a3 >>= ep;
+        a0 += __shfl_xor_sync(kFull, a0, 8);  a1 += __shfl_xor_sync(kFull, a1, 8);
+        a2 += __shfl_xor_sync(kFull, a2, 8);  a3 += __shfl_xor_sync(kFull, a3, 8);
+        a0 += __shfl_xor_sync(kFull, a0, 16); a1 += __shfl_xor_sync(kFull, a1, 16);
+        a2 += __shfl_xor_sync(kFull, a2, 16); a3 += __shfl_xor_sync(kFull, a3, 16);
+        if constexpr (MODE >= 1) {
+            c0 >>= ep; c1 >>= ep;
+            c0 += __shfl_xor_sync(kFull, c0, 8);  c1 += __shfl_xor_sync(kFull, c1, 8);
+            c0 += __shfl_xor_sync(kFull, c0, 16); c1 += __shfl_xor_sync(kFull, c1, 16);
+        }
+        if constexpr (MODE == 2) {
+            c2 >>= ep; c3 >>= ep;
+            c2 += __shfl_xor_sync(kFull, c2, 8);  c3 += __shfl_xor_sync(kFull, c3, 8);
+            c2 += __shfl_xor_sync(kFull, c2, 16); c3 += __shfl_xor_sync(kFull, c3, 16);
+        }
+        *epoch = (ep + 1) & 3;
+        const uint32_t w0 = r0 == 0 ? a0 : c0, w1 = r0 == 0 ? a1 : c1;
+        const uint32_t w2 = r0 == 0 ? a2 : c2, w3 = r0 == 0 ? a3 : c3;
+        cnt[0] = ucols_layer<MODE>(lane, 0) < L ? (uint32_t)__dp4a(w0, 0x01010101u, 0u) : 0u;
+        cnt[1] = ucols_layer<MODE>(lane, 1) < L ? (uint32_t)__dp4a(w1, 0x01010101u, 0u) : 0u;
+        cnt[2] = ucols_layer<MODE>(lane, 2) < L ? (uint32_t)__dp4a(w2, 0x01010101u, 0u) : 0u;
+        cnt[3] = ucols_layer<MODE>(lane, 3) < L ? (uint32_t)__dp4a(w3, 0x01010101u, 0u) : 0u;
+        if (__any_sync(kFull, badw & 0x80808080u)) {
+            status |= EVICT_TREE_BAD_EXPERT;
+            cnt[0] = cnt[1] = cnt[2] = cnt[3] = 0u;
+        }
+    }
+    // union counts (zeros for an errored tree)
+    int32_t *uc = union_count + (size_t)b * L;
+#pragma unroll
+    for (int m = 0; m < 4; m++) {
+        const int l = ucols_layer<MODE>(lane, m);
+        if (l < L) uc[l] = (int)cnt[m];
+    }
+    const int tot = __reduce_add_sync(kFull, (int)(cnt[0] + cnt[1] + cnt[2] + cnt[3]));
+    if (union_total && lane == 0) union_total[b] = tot;
+    if (lsum && status == 0) {
+#pragma unroll
+        for (int m = 0; m < 4; m++) lsum[m] += cnt[m];
+    }
+}
+
 // Dispatch: flags for top-8 ids, register OR for 1/2/4-word masks, generic otherwise.
 template <int NPL, int IDF, int KT, int EW, int R>
 __device__ __forceinline__ void tree_union(uint32_t &status, const uint8_t *__restrict__ klist, int k, int b,

@@ -493,3 +493,40 @@ def test_fused_reads_pinned_host_routing(ev, B):
     torch.cuda.synchronize()
     for k in ("k_star", "keep_bits", "union_count", "union_total", "status", "verify_offsets"):
         assert (a[k] == b[k]).all(), k
+
+
+@pytest.mark.parametrize("L,policy", [(7, None), (20, ("fixed", 45)), (32, None), (33, ("fixed", 40)),
+                                      (40, None), (48, ("fixed", 50)), (48, ("coverage", 0.9)),
+                                      (56, None), (64, ("fixed", 45))])
+def test_throughput_union_emit_modes(ev, L, policy):
+    """The throughput path's union/emit kernel (k_union_emit, B > 2048, u8 top-8, E = 128, N ≤ 64)
+    in its three flag-region layouts (L ≤ 32; 32 < L ≤ 48 half-layer columns; L ≤ 64 layer
+    columns), ragged trees, kept sets reaching nodes ≥ 32 (fixed k / coverage policies: the emit's
+    second node half), an errored tree (NaN q) and a BAD_EXPERT row; A9 statistics folded into
+    the launch must equal the oracle's batch_stats over the call's own outputs."""
+    c = gen.CONFIGS["c2"]
+    B, N, E, K = 4500, c["N"], 128, 8
+    P, Q, n = gen.trees(c["seed"] + L, B, N, c["steps"], c["topk"])
+    n[::5] = np.maximum(1, n[::5] // 3)
+    Q = Q.copy()
+    Q[11, 1] = np.nan                                     # BAD_PROB
+    cost = gen.cost_table(N)
+    ids = gen.routing(c["seed"] + L, B, N, L, E, K)
+    ids[29, 0, L - 1, 5] = 200                            # root is always kept: BAD_EXPERT
+    g = npy(ev.evict_select_build_union(T(P), T(Q), T(cost), T(ids), E, n_nodes=T(n), policy=policy,
+                                        with_stats=True))
+    assert g["status"][11] != 0 and g["status"][29] == 0x10
+    o = oracle.select(P, Q, cost, n_nodes=n, threads=8, policy=policy)
+    res, msgs = compare_select(o, dict(g, status=g["status"] & ~np.uint32(0x10)), n_nodes=n)
+    assert not msgs, msgs[:5]
+    keep = downstream_keep(o, g)
+    if policy is not None and policy[0] == "fixed":
+        assert (g["k_star"] > 32).sum() > 100            # the emit's second half is exercised
+    ou = oracle.expert_union(keep, ids, E, n_nodes=n, threads=8)
+    assert not compare_union(ou, {k: v for k, v in g.items() if k in ("union_count", "union_total")})
+    ob = oracle.build_verify_tree(P, keep, n_nodes=n)
+    assert not compare_build(ob, {k: v for k, v in g.items() if k != "status"})
+    s, d = oracle.batch_stats(N, L, g["k_star"], g["e_hat"].astype(np.float64), g["utility"].astype(np.float64),
+                              g["union_count"], g["status"].astype(np.uint32), n_nodes=n)
+    assert (g["stats"] == s).all(), np.flatnonzero(g["stats"] != s)[:5]
+    assert np.allclose(g["dstats"], d, rtol=1e-9)
