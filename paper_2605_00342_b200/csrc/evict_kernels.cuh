@@ -425,7 +425,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     // only for that configuration; it runs evict_batch_stats after the launch otherwise)
     constexpr bool kFold = LEAN && EW == 2 && CL <= 4;
     const bool fstats = kFold && out.stats != nullptr;
-    uint32_t lsum[4] = {0u, 0u, 0u, 0u};   // folded A9: this lane's layers ucols_layer(lane, m)
+    uint32_t lsum[4] = {0u, 0u, 0u, 0u};   // folded A9: this lane's output layers ulane.l0 + m
+    const UColsLane ulane = ucols_lane<CL == 4 ? 2 : 1>(lane, rt.num_layers);
     if constexpr (kFold) {
         if (fstats) {
             uint32_t *z = reinterpret_cast<uint32_t *>(fs);
@@ -551,7 +552,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                     // lane-owned flag columns (conflict-free byte stores); CL = 3: L ≤ 48, CL = 4: L ≤ 64
                     tree_union_cols<CL == 4 ? 2 : 1, WT == 1 ? 8 : 4>(st, er.klist, er.k, b, N, L, rt.ids, wscr,
                                                                    out.union_count, out.union_total, &epoch,
-                                                                   fstats ? lsum : nullptr);
+                                                                   fstats ? lsum : nullptr, ulane);
                     if constexpr (kFold) {
                         if (fstats && lane == 0) {
                             unsigned *wsc = fs->sc[warp];
@@ -624,10 +625,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
         if (fstats) {
             // per-lane layer sums (tree_union_cols' output layers)
 #pragma unroll
-            for (int m = 0; m < 4; m++) {
-                const int l = ucols_layer<CL == 4 ? 2 : 1>(lane, m);
-                if (l < L && lsum[m]) atomicAdd(&fs->lay[l], lsum[m]);
-            }
+            for (int m = 0; m < 4; m++)
+                if (m < ulane.nl && lsum[m]) atomicAdd(&fs->lay[ulane.l0 + m], lsum[m]);
             __syncthreads();
             unsigned long long *gs = reinterpret_cast<unsigned long long *>(out.stats);
             if (threadIdx.x == 0) {

@@ -1354,21 +1354,33 @@ __device__ __forceinline__ void tree_union_flags64(uint32_t &status, const uint8
 // slot layout of tree_union_flags64 puts the two halves of a layer on one bank group, ≈ 2
 // wavefronts per store).  The store offset of id e is one PRMT of two per-word vectors:
 // lo = (w & 0x03030303) | column base, hi = (w >> 2) & 0x1F1F1F1F give (e >> 2) << 8 | lo.
-// Marker epochs as in tree_union_flags64 (tree t stores 1 << (t mod 4), the block is cleared
-// after every 4th read-back).  Read-back: lane (q = lane & 7, r0 = lane >> 3) loads rows r0 + 4j
-// (j < 8) as 16-byte vectors (8 lanes per 128-byte phase: conflict-free), sums marker bits
-// bytewise per column, two xor-shuffles over r0, one IDP4A per layer.  Lane outputs: layers
-// ue_lanes_layer(lane, m) (lanes 0–7 region 0, lanes 8–15 region 1; 64 = none).
+// Nibble markers: tree t stores 0x01 (t even) or 0x10 (t odd) and the block is cleared after
+// every second read-back, so a byte holds at most one marker of each parity and 8-row byte
+// sums keep the two parities in separate nibbles (≤ 8 each): the read-back adds raw words.
+// Read-back: lane (q = lane & 7, r0 = lane >> 3) loads rows r0 + 4j (j < 8) as 16-byte vectors
+// (8 lanes per 128-byte phase: conflict-free), sums per column, keeps its parity's nibbles, two
+// xor-shuffles over r0, one IDP4A per layer.
+// Lane outputs (UColsLane, computed once per kernel): lanes 0–7 region 0 layers 4q..4q+3,
+// lanes 8–15 region 1 (MODE 1: 32 + 2q, 33 + 2q; MODE 2: 32 + 4q..), others none.
+struct UColsLane {
+    int l0;          // first output layer (64: none)
+    int nl;          // output layers of this lane (0, 2 or 4), all < L
+    bool vec;        // one 8/16-byte store covers them (contiguous, aligned)
+};
 template <int MODE>
-__device__ __forceinline__ int ucols_layer(int lane, int m)
+__device__ __forceinline__ UColsLane ucols_lane(int lane, int L)
 {
     const int q = lane & 7, r0 = lane >> 3;
-    if (r0 == 0) return 4 * q + m;
-    if (r0 == 1) {
-        if constexpr (MODE == 1) return m < 2 ? 32 + 2 * q + m : 64;
-        if constexpr (MODE == 2) return 32 + 4 * q + m;
-    }
-    return 64;
+    UColsLane u{64, 0, false};
+    if (r0 == 0) { u.l0 = 4 * q; u.nl = 4; }
+    else if (r0 == 1 && MODE == 1) { u.l0 = 32 + 2 * q; u.nl = 2; }
+    else if (r0 == 1 && MODE == 2) { u.l0 = 32 + 4 * q; u.nl = 4; }
+    int n = L - u.l0;
+    n = n < 0 ? 0 : (n > u.nl ? u.nl : n);
+    u.vec = n == u.nl && n > 0 && (L % u.nl) == 0;   // b·L + l0 is a multiple of nl
+    u.nl = n;
+    if (n == 0) u.l0 = 64;
+    return u;
 }
 __device__ __forceinline__ uint32_t prmt_b32(uint32_t a, uint32_t b, uint32_t sel)
 {
@@ -1391,15 +1403,15 @@ __device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t 
                                                 int b, int N, int L, const void *__restrict__ ids,
                                                 uint8_t *flags, int32_t *__restrict__ union_count,
                                                 int32_t *__restrict__ union_total, int *epoch,
-                                                uint32_t *lsum)
+                                                uint32_t *lsum, const UColsLane &ul)
 {
     const int lane = lane_id();
     const int q = lane & 7, r0 = lane >> 3;
     const bool run = status == 0 && k > 0;
     uint32_t cnt[4] = {0u, 0u, 0u, 0u};
     if (run) {
-        const int ep = *epoch;
-        const uint32_t marker = 1u << ep;
+        const int ep = *epoch;                      // 0 or 1
+        const uint32_t marker = ep ? 0x10u : 0x01u;
         const uint32_t fb = (uint32_t)__cvta_generic_to_shared(flags);
         const uint32_t rowB = (uint32_t)L * 8u;
         // lanes past the layers re-read byte 0 of the row: their flags land in columns of
@@ -1411,6 +1423,7 @@ __device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t 
         const uint32_t cb0 = (4u * (uint32_t)lane) * 0x01010101u;
         const uint32_t cb1 = (128u + 4u * (uint32_t)lane) * 0x01010101u;
         const uint8_t *tb = reinterpret_cast<const uint8_t *>(ids) + (size_t)b * N * rowB;
+        const uint8_t *p0 = tb + lo0, *p1 = tb + lo1;
         uint32_t badw = 0u;
 #pragma unroll 1
         for (int j0 = 0; j0 < k; j0 += UB) {
@@ -1418,14 +1431,14 @@ __device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t 
             uint32_t x1[UB], x2[UB];
 #pragma unroll
             for (int u = 0; u < UB; u++) {
-                const uint8_t *rp = tb + (uint32_t)klist[min(j0 + u, k - 1)] * rowB;
-                x0[u] = __ldg(reinterpret_cast<const uint2 *>(rp + lo0));
+                const uint32_t o = (uint32_t)klist[min(j0 + u, k - 1)] * rowB;
+                x0[u] = __ldg(reinterpret_cast<const uint2 *>(p0 + o));
                 x1[u] = 0u;
                 x2[u] = 0u;
                 if constexpr (MODE == 1) {
-                    x1[u] = __ldg(reinterpret_cast<const uint32_t *>(rp + lo1));
+                    x1[u] = __ldg(reinterpret_cast<const uint32_t *>(p1 + o));
                 } else if constexpr (MODE == 2) {
-                    const uint2 y = __ldg(reinterpret_cast<const uint2 *>(rp + lo1));
+                    const uint2 y = __ldg(reinterpret_cast<const uint2 *>(p1 + o));
                     x1[u] = y.x;
                     x2[u] = y.y;
                 }
@@ -1446,61 +1459,62 @@ __device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t 
             }
         }
         __syncwarp();
-        const uint32_t mk = 0x01010101u << ep;
-        const bool clear = ep == 3;
+        const bool clear = ep == 1;
         uint32_t a0 = 0u, a1 = 0u, a2 = 0u, a3 = 0u, c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u;
 #pragma unroll
         for (int j = 0; j < 8; j++) {
             const uint32_t ra = fb + 256u * (uint32_t)(r0 + 4 * j) + 16u * (uint32_t)q;
             const uint4 x = lds_v4(ra);
-            a0 += x.x & mk; a1 += x.y & mk; a2 += x.z & mk; a3 += x.w & mk;
+            a0 += x.x; a1 += x.y; a2 += x.z; a3 += x.w;
             if constexpr (MODE == 1) {
                 const uint4 y = lds_v4(ra + 128u);
-                c0 += (y.x | y.y) & mk;   // layer 32 + 2q (both halves)
-                c1 += (y.z | y.w) & mk;   // layer 33 + 2q
+                c0 += y.x | y.y;   // layer 32 + 2q (both halves)
+                c1 += y.z | y.w;   // layer 33 + 2q
             } else if constexpr (MODE == 2) {
                 const uint4 y = lds_v4(ra + 128u);
-                c0 += y.x & mk; c1 += y.y & mk; c2 += y.z & mk; c3 += y.w & mk;
+                c0 += y.x; c1 += y.y; c2 += y.z; c3 += y.w;
             }
             if (clear) {
                 sts_v4_zero(ra);
                 if constexpr (MODE >= 1) sts_v4_zero(ra + 128u);
             }
         }
-        // ≤ 8 markers per byte after the shift; the sum over the 4 lanes of a column quad ≤ 32
-        a0 >>= ep; a1 >>= ep; a2 >>= ep; a3 >>= ep;
-        a0 += __shfl_xor_sync(kFull, a0, 8);  a1 += __shfl_xor_sync(kFull, a1, 8);
-        a2 += __shfl_xor_sync(kFull, a2, 8);  a3 += __shfl_xor_sync(kFull, a3, 8);
-        a0 += __shfl_xor_sync(kFull, a0, 16); a1 += __shfl_xor_sync(kFull, a1, 16);
-        a2 += __shfl_xor_sync(kFull, a2, 16); a3 += __shfl_xor_sync(kFull, a3, 16);
-        if constexpr (MODE >= 1) {
-            c0 >>= ep; c1 >>= ep;
-            c0 += __shfl_xor_sync(kFull, c0, 8);  c1 += __shfl_xor_sync(kFull, c1, 8);
-            c0 += __shfl_xor_sync(kFull, c0, 16); c1 += __shfl_xor_sync(kFull, c1, 16);
-        }
-        if constexpr (MODE == 2) {
-            c2 >>= ep; c3 >>= ep;
-            c2 += __shfl_xor_sync(kFull, c2, 8);  c3 += __shfl_xor_sync(kFull, c3, 8);
-            c2 += __shfl_xor_sync(kFull, c2, 16); c3 += __shfl_xor_sync(kFull, c3, 16);
-        }
-        *epoch = (ep + 1) & 3;
-        const uint32_t w0 = r0 == 0 ? a0 : c0, w1 = r0 == 0 ? a1 : c1;
-        const uint32_t w2 = r0 == 0 ? a2 : c2, w3 = r0 == 0 ? a3 : c3;
-        cnt[0] = ucols_layer<MODE>(lane, 0) < L ? (uint32_t)__dp4a(w0, 0x01010101u, 0u) : 0u;
-        cnt[1] = ucols_layer<MODE>(lane, 1) < L ? (uint32_t)__dp4a(w1, 0x01010101u, 0u) : 0u;
-        cnt[2] = ucols_layer<MODE>(lane, 2) < L ? (uint32_t)__dp4a(w2, 0x01010101u, 0u) : 0u;
-        cnt[3] = ucols_layer<MODE>(lane, 3) < L ? (uint32_t)__dp4a(w3, 0x01010101u, 0u) : 0u;
+        *epoch = ep ^ 1;
+        // this lane's words (its output region), this parity's nibbles: ≤ 8 per byte, ≤ 32 after
+        // the sum over the 4 lanes (r0) of a column quad
+        const int sh = 4 * ep;
+        uint32_t w0 = ((r0 & 1) ? c0 : a0) >> sh & 0x0F0F0F0Fu, w1 = ((r0 & 1) ? c1 : a1) >> sh & 0x0F0F0F0Fu;
+        uint32_t w2 = ((r0 & 1) ? c2 : a2) >> sh & 0x0F0F0F0Fu, w3 = ((r0 & 1) ? c3 : a3) >> sh & 0x0F0F0F0Fu;
+        // partners across r0 hold the other region's words for odd r0: exchange both regions
+        uint32_t o0 = ((r0 & 1) ? a0 : c0) >> sh & 0x0F0F0F0Fu, o1 = ((r0 & 1) ? a1 : c1) >> sh & 0x0F0F0F0Fu;
+        uint32_t o2 = ((r0 & 1) ? a2 : c2) >> sh & 0x0F0F0F0Fu, o3 = ((r0 & 1) ? a3 : c3) >> sh & 0x0F0F0F0Fu;
+        // xor 8 swaps r0 parity: the partner's "other" words are this lane's region
+        w0 += __shfl_xor_sync(kFull, o0, 8); w1 += __shfl_xor_sync(kFull, o1, 8);
+        w2 += __shfl_xor_sync(kFull, o2, 8); w3 += __shfl_xor_sync(kFull, o3, 8);
+        w0 += __shfl_xor_sync(kFull, w0, 16); w1 += __shfl_xor_sync(kFull, w1, 16);
+        w2 += __shfl_xor_sync(kFull, w2, 16); w3 += __shfl_xor_sync(kFull, w3, 16);
+        cnt[0] = (uint32_t)__dp4a(w0, 0x01010101u, 0u);
+        cnt[1] = (uint32_t)__dp4a(w1, 0x01010101u, 0u);
+        cnt[2] = (uint32_t)__dp4a(w2, 0x01010101u, 0u);
+        cnt[3] = (uint32_t)__dp4a(w3, 0x01010101u, 0u);
         if (__any_sync(kFull, badw & 0x80808080u)) {
             status |= EVICT_TREE_BAD_EXPERT;
             cnt[0] = cnt[1] = cnt[2] = cnt[3] = 0u;
         }
     }
     // union counts (zeros for an errored tree)
-    int32_t *uc = union_count + (size_t)b * L;
+    if (ul.nl < 4) cnt[3] = 0u;
+    if (ul.nl < 3) cnt[2] = 0u;
+    if (ul.nl < 2) cnt[1] = 0u;
+    if (ul.nl < 1) cnt[0] = 0u;
+    int32_t *uc = union_count + (size_t)b * L + ul.l0;
+    if (ul.vec) {
+        if (ul.nl == 4) *reinterpret_cast<int4 *>(uc) = make_int4((int)cnt[0], (int)cnt[1], (int)cnt[2], (int)cnt[3]);
+        else *reinterpret_cast<int2 *>(uc) = make_int2((int)cnt[0], (int)cnt[1]);
+    } else {
 #pragma unroll
-    for (int m = 0; m < 4; m++) {
-        const int l = ucols_layer<MODE>(lane, m);
-        if (l < L) uc[l] = (int)cnt[m];
+        for (int m = 0; m < 4; m++)
+            if (m < ul.nl) uc[m] = (int)cnt[m];
     }
     const int tot = __reduce_add_sync(kFull, (int)(cnt[0] + cnt[1] + cnt[2] + cnt[3]));
     if (union_total && lane == 0) union_total[b] = tot;
