@@ -421,7 +421,9 @@ __device__ __forceinline__ void g_rank_argmax(GTree<G> &t, uint8_t *rk, const fl
 // first k* nodes: every node with score > v (v = the k*-th largest score) plus
 // the k* − #{score > v} lowest-index nodes with score == v.  prefix_row may be
 // written (values only).
-template <int G>
+// COST: the launch's policy is EVICT_POLICY_COST (k* = smallest argmax of the ratio; no coverage
+// or fixed-k test per position)
+template <int G, bool COST = false>
 __device__ __forceinline__ void g_select_values(GTree<G> &t, const float (&c)[NP], int N,
                                                 float *__restrict__ prefix_row, const evict_policy_t &pol)
 {
@@ -488,19 +490,27 @@ __device__ __forceinline__ void g_select_values(GTree<G> &t, const float (&c)[NP
         best = Rb[r] > best ? Rb[r] : best;
     }
     const uint32_t mx = g_max<G>(best);
-    float SK = 0.f;   // S at position n−1 (coverage policy)
-    if (pol.kind == EVICT_POLICY_COVERAGE) {
-        float sl = 0.f;
-#pragma unroll
-        for (int r = 0; r < NP; r++)
-            if (base + r == t.n - 1) sl = S[r];
-        const int own = ok && t.n >= 1 ? (t.n - 1) / NP : 0;
-        SK = __shfl_sync(kFull, sl, (threadIdx.x & 31 & ~(G - 1)) + own);
-    }
     int rfirst = NP;
+    if constexpr (COST) {
+        // Rb = 0 past n and for an errored tree: only valid positions can equal mx > 0; mx = 0
+        // (every ratio 0) takes position 0
 #pragma unroll
-    for (int r = NP - 1; r >= 0; r--)
-        if (ok && base + r < t.n && policy_hit(pol, base + r, t.n, Rb[r], mx, S[r], SK)) rfirst = r;
+        for (int r = NP - 1; r >= 0; r--)
+            if (Rb[r] == mx && (mx != 0u || base + r == 0)) rfirst = r;
+    } else {
+        float SK = 0.f;   // S at position n−1 (coverage policy)
+        if (pol.kind == EVICT_POLICY_COVERAGE) {
+            float sl = 0.f;
+#pragma unroll
+            for (int r = 0; r < NP; r++)
+                if (base + r == t.n - 1) sl = S[r];
+            const int own = ok && t.n >= 1 ? (t.n - 1) / NP : 0;
+            SK = __shfl_sync(kFull, sl, (threadIdx.x & 31 & ~(G - 1)) + own);
+        }
+#pragma unroll
+        for (int r = NP - 1; r >= 0; r--)
+            if (ok && base + r < t.n && policy_hit(pol, base + r, t.n, Rb[r], mx, S[r], SK)) rfirst = r;
+    }
     const unsigned has = __ballot_sync(kFull, rfirst < NP);
     const unsigned gm = (G == 32) ? has : ((has >> (gidx<G>() * G)) & ((1u << G) - 1u));
     const int wl = gm ? __ffs(gm) - 1 : 0;                 // smallest k wins ties (Z3)
@@ -548,10 +558,12 @@ __device__ __forceinline__ void g_select_values(GTree<G> &t, const float (&c)[NP
     int take = kstar - ngt - eq_before;                    // ties this lane may keep
     take = take < 0 ? 0 : (take > neq ? neq : take);
     uint32_t keq = eq;
+    if (neq > take) {   // rare: more ties at the cut than slots left in this lane
 #pragma unroll
-    for (int r = 0; r < NP; r++) {
-        // drop the highest set bits beyond `take`
-        if (__popc(keq) > take) keq &= ~(0x80000000u >> __clz(keq));
+        for (int r = 0; r < NP; r++) {
+            // drop the highest set bits beyond `take`
+            if (__popc(keq) > take) keq &= ~(0x80000000u >> __clz(keq));
+        }
     }
     const uint32_t kb = ok ? (gt | keq) : 0u;
     uint64_t local[W];

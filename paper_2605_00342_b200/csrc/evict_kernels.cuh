@@ -493,10 +493,19 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 for (int r = 0; r < grp::NP; r++) pw[r >> 2] |= (uint32_t)(t.par[r] & 0xff) << (8 * (r & 3));
                 *reinterpret_cast<uint2 *>(&er.par[base]) = make_uint2(pw[0], pw[1]);
                 if (g < W) er.keep[g] = t.keep[g];
+                if constexpr (W == 1) {
+                    // this lane's 8 keep bits and the slot of its first node: 32-bit work per node
+                    const uint32_t kb = (uint32_t)(t.keep[0] >> base) & 0xffu & ((t.n - base) >= grp::NP ? 0xffu : ((1u << (t.n - base > 0 ? t.n - base : 0)) - 1u));
+                    const int sb = __popcll(t.keep[0] & ((1ull << base) - 1ull));
 #pragma unroll
-                for (int r = 0; r < grp::NP; r++) {
-                    const int i = base + r;
-                    if (i < t.n && grp::bit_w<W>(t.keep, i)) er.klist[grp::popc_below_w<W>(t.keep, i)] = (uint8_t)i;
+                    for (int r = 0; r < grp::NP; r++)
+                        if ((kb >> r) & 1u) er.klist[sb + __popc(kb & ((1u << r) - 1u))] = (uint8_t)(base + r);
+                } else {
+#pragma unroll
+                    for (int r = 0; r < grp::NP; r++) {
+                        const int i = base + r;
+                        if (i < t.n && grp::bit_w<W>(t.keep, i)) er.klist[grp::popc_below_w<W>(t.keep, i)] = (uint8_t)i;
+                    }
                 }
                 if (g == 0) { er.n = t.n; er.k = k; er.status = t.status; er.ehat = t.ehat; er.util = t.util; }
             } else if (g == 0 && slot < WT) {
@@ -713,7 +722,7 @@ static __global__ void __launch_bounds__(1024) k_scan_offsets(int B, const int32
     }
 }
 
-template <int G>
+template <int G, bool COST = false>   // COST: the policy is EVICT_POLICY_COST (compile-time argmax epilogue)
 __global__ void __launch_bounds__(kSelWarps * 32) k_select_g(evict_trees_t tr, const float *cost,
                                                              int cost_stride, evict_policy_t pol, int32_t *k_star,
                                                              float *e_hat, float *utility,
@@ -745,7 +754,7 @@ __global__ void __launch_bounds__(kSelWarps * 32) k_select_g(evict_trees_t tr, c
     int32_t *orow = (active && order) ? order + (size_t)b * N : nullptr;
     float *prow = (active && prefix_sums) ? prefix_sums + (size_t)b * N : nullptr;
     if (order) grp::g_rank_argmax<G>(t, rk_all + slot * NMAX, c, N, orow, prow, pol);   // kernel-uniform
-    else grp::g_select_values<G>(t, c, N, prow, pol);
+    else grp::g_select_values<G, COST>(t, c, N, prow, pol);
     if (chunk_sums) {
         // packed verify-row offsets, first half: Σk* per chunk of kScanChunk trees (one atomic
         // per CTA); k_scan_offsets turns the chunk sums and k* into the exclusive scan
@@ -942,9 +951,9 @@ struct FusedLauncher {
                     constexpr int PER = kSelWarps * grp::GShape<G>::TPW;
                     const int sblocks = (tr->batch + PER - 1) / PER;
                     int32_t *chunk_sums = reinterpret_cast<int32_t *>(ws + 1);   // zeroed by the caller
-                    k_select_g<G><<<sblocks, kSelWarps * 32, 0, s>>>(*tr, cost, cs, pol, o->k_star, o->e_hat,
-                                                                    o->utility, o->keep_bits, nullptr, nullptr,
-                                                                    o->status, chunk_sums);
+                    auto sk = pol.kind == EVICT_POLICY_COST ? k_select_g<G, true> : k_select_g<G, false>;
+                    sk<<<sblocks, kSelWarps * 32, 0, s>>>(*tr, cost, cs, pol, o->k_star, o->e_hat, o->utility,
+                                                         o->keep_bits, nullptr, nullptr, o->status, chunk_sums);
                     k_scan_offsets<<<(tr->batch + kScanChunk - 1) / kScanChunk, 1024, 0, s>>>(
                         tr->batch, o->k_star, chunk_sums, o->verify_offsets);
                     if (cudaGetLastError() != cudaSuccess) return EVICT_ERR_CUDA;
@@ -984,8 +993,9 @@ evict_status_t launch_select(const evict_trees_t *tr, const float *cost, int cs,
     constexpr int G = NPL == 2 ? 8 : 16;
     constexpr int per_cta = kSelWarps * grp::GShape<G>::TPW;
     const int blocks = (tr->batch + per_cta - 1) / per_cta;
-    k_select_g<G><<<blocks, kSelWarps * 32, 0, s>>>(*tr, cost, cs, pol, k_star, e_hat, utility, keep_bits,
-                                                      order, prefix_sums, status);
+    auto sk = (pol.kind == EVICT_POLICY_COST && !order) ? k_select_g<G, true> : k_select_g<G, false>;
+    sk<<<blocks, kSelWarps * 32, 0, s>>>(*tr, cost, cs, pol, k_star, e_hat, utility, keep_bits,
+                                                      order, prefix_sums, status, nullptr);
     return launched();
 }
 
