@@ -233,13 +233,16 @@ __device__ __forceinline__ void g_levels(GTree<G> &t, float *sd)
 {
     const int g = gl<G>();
     const int base = g * NP;
-    bool live[NP];
+    // non-live nodes (root, pads, errored tree) read the root's slot (always 1) times 1: their
+    // score stays 1 without a select per sweep
     int pidx[NP];
+    float qe[NP];
 #pragma unroll
     for (int r = 0; r < NP; r++) {
         const int i = base + r;
-        live[r] = (t.status == 0) && (i > 0) && (i < t.n);
-        pidx[r] = live[r] ? swz(t.par[r]) : 0;
+        const bool live = (t.status == 0) && (i > 0) && (i < t.n);
+        pidx[r] = live ? swz(t.par[r]) : 0;
+        qe[r] = live ? t.q[r] : 1.f;
         t.sc[r] = 1.f;
     }
     const int c0 = swz(base), c1 = swz(base + 4);
@@ -248,14 +251,14 @@ __device__ __forceinline__ void g_levels(GTree<G> &t, float *sd)
     __syncwarp();
     if constexpr (SCORES) {
         while (true) {
-            bool changed = false;
+            uint32_t diff = 0u;
             float ns[NP];
 #pragma unroll
             for (int r = 0; r < NP; r++) {
-                const float sv = __fmul_rn(sd[pidx[r]], t.q[r]);   // both ≥ +0
-                ns[r] = live[r] ? sv : t.sc[r];
-                changed |= __float_as_int(ns[r]) != __float_as_int(t.sc[r]);
+                ns[r] = __fmul_rn(sd[pidx[r]], qe[r]);   // both ≥ +0
+                diff |= __float_as_uint(ns[r]) ^ __float_as_uint(t.sc[r]);
             }
+            const bool changed = diff != 0u;
             __syncwarp();
 #pragma unroll
             for (int r = 0; r < NP; r++) t.sc[r] = ns[r];
@@ -586,6 +589,8 @@ __device__ __forceinline__ void g_select_values(GTree<G> &t, const float (&c)[NP
 //      next-sibling from the child masks and emits the packed row.
 // par: the tree's shared parent record; klist: its kept nodes (built by the select); child (NMAX × W words)
 // (all in shared memory).
+// slot_of (optional, N ≤ 64): node → slot for the kept nodes (built with klist) — one byte load per
+// ancestor step instead of a 64-bit masked popcount.
 template <int G>
 __device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W], int n, bool emit,
                                        int k, int b, int N, int off, int pos_off,
@@ -595,9 +600,47 @@ __device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W]
                                        int32_t *__restrict__ positions,
                                        int32_t *__restrict__ next_token,
                                        int32_t *__restrict__ next_sibling,
-                                       uint64_t *__restrict__ tree_mask)
+                                       uint64_t *__restrict__ tree_mask, const uint8_t *slot_of = nullptr)
 {
     constexpr int W = GShape<G>::W;
+    if constexpr (W == 1) {
+        if (slot_of != nullptr) {
+            const int g = gl<G>();
+            const int kk = emit ? k : 0;
+            for (int s = g; s < kk; s += G) child[s] = 0ull;
+            __syncwarp();
+            for (int s = g; s < kk; s += G) {
+                const int i = klist[s];
+                if (i > 0)
+                    atomicOr(reinterpret_cast<unsigned long long *>(&child[slot_of[par[i]]]), 1ull << s);
+            }
+            __syncwarp();
+            for (int s = g; s < kk; s += G) {
+                const int i = klist[s];
+                uint64_t row = 1ull << s;
+                int depth = 0;
+                for (int a = par[i]; a >= 0; a = par[a]) {   // strict ancestors, all kept
+                    depth++;
+                    row |= 1ull << slot_of[a];
+                }
+                const uint64_t cm = child[s];
+                const int nt = cm ? __ffsll((long long)cm) - 1 : -1;
+                int ns = -1;
+                if (i > 0) {
+                    const uint64_t sib = child[slot_of[par[i]]] & (s >= 63 ? 0ull : (~0ull << (s + 1)));
+                    ns = sib ? __ffsll((long long)sib) - 1 : -1;
+                }
+                const int rowi = off + s;
+                if (kept_index) kept_index[rowi] = i;
+                if (retrieve_index) retrieve_index[rowi] = b * N + i;
+                if (positions) positions[rowi] = pos_off + depth;
+                if (next_token) next_token[rowi] = nt;
+                if (next_sibling) next_sibling[rowi] = ns;
+                if (tree_mask) tree_mask[rowi] = row;
+            }
+            return;
+        }
+    }
     const int g = gl<G>();
     const int base = g * NP;
     const int kk = emit ? k : 0;

@@ -21,6 +21,10 @@
 #include "evict_group.cuh"
 #include "evict_launch.h"
 
+#ifndef EVICT_UCOLS_UB
+#define EVICT_UCOLS_UB 4   // kept rows per load batch of tree_union_cols (8 measured slower)
+#endif
+
 namespace evict {
 
 // ------------------------------------------------------------ tile scan
@@ -339,6 +343,7 @@ struct EmitRec {
     uint64_t keep[W];
     alignas(8) int8_t par[NMAX];
     alignas(8) uint8_t klist[NMAX];   // kept nodes, ascending (slot order), built once in A1
+    alignas(8) uint8_t slot[NMAX];    // node → slot for kept nodes (W = 1 only: the emit's ancestor walk)
     int n, k;
     uint32_t status;
     float ehat, util;                 // for the folded A9 statistics
@@ -380,12 +385,12 @@ __host__ __device__ inline size_t fused_scratch_bytes(int L, int E, bool flags)
     const size_t x = fused_scratch_fixed<G>();
     return align16(f > x ? f : x);
 }
-template <int G, int WT = kWT>
-__host__ __device__ inline size_t fused_smem_bytes(int L, int E, bool flags)
+template <int G, int WT = kWT, int NW = kWarps>
+__host__ __device__ inline size_t fused_smem_bytes(int L, int E, bool flags, bool ranks = true)
 {
-    return (size_t)kWarps * fused_scratch_bytes<G>(L, E, flags)          // scratch
-           + align16(sizeof(EmitRec<G>) * kWarps * WT)                   // records
-           + align16((size_t)kWarps * grp::GShape<G>::TPW * grp::GShape<G>::NMAX)  // ranks (order row)
+    return (size_t)NW * fused_scratch_bytes<G>(L, E, flags)              // scratch
+           + align16(sizeof(EmitRec<G>) * NW * WT)                       // records
+           + (ranks ? align16((size_t)NW * grp::GShape<G>::TPW * grp::GShape<G>::NMAX) : 0)  // ranks (order row)
            + kStatsSmem;                                                  // folded A9 statistics
 }
 
@@ -395,8 +400,11 @@ __host__ __device__ inline size_t fused_smem_bytes(int L, int E, bool flags)
 // PRE (two-kernel throughput path, LEAN only): k_select_g already wrote k*, e_hat, utility, keep
 // bits, select status and the packed offsets (scanned in the same launch); this kernel rebuilds
 // each tree's emit record from them (parent row, keep bits) and runs A6 + A7 (+ A9) only.
-template <int NPL, int IDF, int KT, int EW, int CL, bool LEAN = false, int WT = kWT, bool PRE = false>
-__global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, const float *cost,
+// NW: warps per CTA — 8, or 4 for the PRE union/emit kernel, whose 4 × 8 KB flag blocks then sit in
+// the first 32 KB of the dynamic shared memory: warp w's byte-store address is the CTA-uniform block
+// base (an STS uniform-register operand) + one PRMT result (tree_union_cols)
+template <int NPL, int IDF, int KT, int EW, int CL, bool LEAN = false, int WT = kWT, bool PRE = false, int NW = kWarps>
+__global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : 3) k_fused(evict_trees_t tr, const float *cost,
                                                        int cost_stride, evict_policy_t pol, evict_routing_t rt,
                                                        evict_fused_out_t out, uint64_t *ws,
                                                        int ntiles)
@@ -416,17 +424,32 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
     const int L = rt.num_layers, E = rt.num_experts;
     const bool do_union = out.union_count != nullptr;
     const size_t scratch = fused_scratch_bytes<G>(L, E, FLAGS && do_union);
-    uint8_t *wscr = dsm + (size_t)warp * scratch;
-    EmitRec<G> *rec = reinterpret_cast<EmitRec<G> *>(dsm + (size_t)kWarps * scratch) + warp * WT;
-    uint8_t *ranks = reinterpret_cast<uint8_t *>(dsm + (size_t)kWarps * scratch) + align16(sizeof(EmitRec<G>) * kWarps * WT);
+    // NW == 4: the 4 scratch (= flag) blocks are static shared memory, so their address is a link-time
+    // constant the compiler folds into every byte store's immediate; the dynamic block holds the rest
+    uint8_t *scr_base = dsm;
+    size_t dyn_scr = (size_t)NW * scratch;
+    if constexpr (NW == 4) {
+        __shared__ __align__(16) uint8_t s_scr4[4 * 8192];
+        scr_base = s_scr4;
+        dyn_scr = 0;
+    }
+    uint8_t *wscr = scr_base + (size_t)warp * scratch;
+    EmitRec<G> *rec = reinterpret_cast<EmitRec<G> *>(dsm + dyn_scr) + warp * WT;
+    uint8_t *ranks = reinterpret_cast<uint8_t *>(dsm + dyn_scr) + align16(sizeof(EmitRec<G>) * NW * WT);
     uint8_t *rk = ranks + ((size_t)warp * TPW + gi) * NMAX;
-    FusedStats *fs = reinterpret_cast<FusedStats *>(ranks + align16((size_t)kWarps * TPW * NMAX));
+    FusedStats *fs = reinterpret_cast<FusedStats *>(ranks + (LEAN ? 0 : align16((size_t)NW * TPW * NMAX)));
     // A9 folded into the launch: the single-pass E = 128 LEAN union (the caller passes out.stats
     // only for that configuration; it runs evict_batch_stats after the launch otherwise)
     constexpr bool kFold = LEAN && EW == 2 && CL <= 4;
     const bool fstats = kFold && out.stats != nullptr;
     uint32_t lsum[4] = {0u, 0u, 0u, 0u};   // folded A9: this lane's output layers ulane.l0 + m
     const UColsLane ulane = ucols_lane<CL == 4 ? 2 : 1>(lane, rt.num_layers);
+    // NW == 4 (the PRE launch: union_count given, E = 128, so every scratch block is the 8 KB flag
+    // block): byte stores at the CTA-uniform base sfold + a PRMT result whose row byte carries 32·warp
+    // (hfold); otherwise at this warp's block (sfold = its address, hfold = 0)
+    constexpr bool fold = NW == 4;
+    const uint32_t sfold = (uint32_t)__cvta_generic_to_shared(fold ? scr_base : wscr);
+    const uint32_t hfold = fold ? (32u * (uint32_t)warp) * 0x01010101u : 0u;
     if constexpr (kFold) {
         if (fstats) {
             uint32_t *z = reinterpret_cast<uint32_t *>(fs);
@@ -499,7 +522,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                     const int sb = __popcll(t.keep[0] & ((1ull << base) - 1ull));
 #pragma unroll
                     for (int r = 0; r < grp::NP; r++)
-                        if ((kb >> r) & 1u) er.klist[sb + __popc(kb & ((1u << r) - 1u))] = (uint8_t)(base + r);
+                        if ((kb >> r) & 1u) {
+                            const int sl = sb + __popc(kb & ((1u << r) - 1u));
+                            er.klist[sl] = (uint8_t)(base + r);
+                            er.slot[base + r] = (uint8_t)sl;
+                        }
                 } else {
 #pragma unroll
                     for (int r = 0; r < grp::NP; r++) {
@@ -559,9 +586,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 uint32_t st = er.status;
                 if constexpr (LEAN && EW == 2 && CL <= 4) {
                     // lane-owned flag columns (conflict-free byte stores); CL = 3: L ≤ 48, CL = 4: L ≤ 64
-                    tree_union_cols<CL == 4 ? 2 : 1, WT == 1 ? 8 : 4>(st, er.klist, er.k, b, N, L, rt.ids, wscr,
+                    tree_union_cols<CL == 4 ? 2 : 1, EVICT_UCOLS_UB>(st, er.klist, er.k, b, N, L, rt.ids, wscr,
                                                                    out.union_count, out.union_total, &epoch,
-                                                                   fstats ? lsum : nullptr, ulane);
+                                                                   fstats ? lsum : nullptr, ulane, sfold, hfold);
                     if constexpr (kFold) {
                         if (fstats && lane == 0) {
                             unsigned *wsc = fs->sc[warp];
@@ -624,7 +651,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             grp::g_emit<G>(keep, active ? er.n : 0, active && k > 0, k, b, N, off,
                            (active && out.pos_offset) ? __ldg(out.pos_offset + b) : 0, er.par,
                            child, er.klist, out.kept_index, out.retrieve_index, out.positions,
-                           out.next_token, out.next_sibling, out.tree_mask);
+                           out.next_token, out.next_sibling, out.tree_mask, W == 1 ? er.slot : nullptr);
             __syncwarp();
         }
         EVICT_PHASE(4);
@@ -641,7 +668,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
             if (threadIdx.x == 0) {
                 unsigned long long su = 0, sc[4] = {0ull, 0ull, 0ull, 0ull};
                 for (int l = 0; l < L; l++) su += fs->lay[l];
-                for (int w = 0; w < kWarps; w++)
+                for (int w = 0; w < NW; w++)
                     for (int i = 0; i < 4; i++) sc[i] += fs->sc[w][i];
                 if (sc[0]) atomicAdd(gs + 0, sc[0]);
                 if (sc[1]) atomicAdd(gs + 1, sc[1]);
@@ -649,7 +676,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) k_fused(evict_trees_t tr, cons
                 if (su) atomicAdd(gs + 3, su);
                 if (sc[3]) atomicAdd(gs + 4, sc[3]);
                 double de = 0.0, du = 0.0;
-                for (int w = 0; w < kWarps; w++) { de += fs->d[w][0]; du += fs->d[w][1]; }
+                for (int w = 0; w < NW; w++) { de += fs->d[w][0]; du += fs->d[w][1]; }
                 atomicAdd(out.dstats + 0, de);
                 atomicAdd(out.dstats + 1, du);
             }
@@ -782,10 +809,10 @@ int dev_sms();  // evict_api.cu
 inline evict_status_t launched() { return cudaGetLastError() == cudaSuccess ? EVICT_OK : EVICT_ERR_CUDA; }
 
 template <typename K>
-inline int persistent_blocks(K kernel, int ntiles, size_t dyn = 0)
+inline int persistent_blocks(K kernel, int ntiles, size_t dyn = 0, int nthreads = kWarps * 32)
 {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarps * 32, dyn);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nthreads, dyn);
     if (per_sm < 1) per_sm = 1;
     long g = (long)dev_sms() * per_sm;
     return (int)(g < ntiles ? g : ntiles);
@@ -963,6 +990,20 @@ struct FusedLauncher {
                         if (rt->num_layers <= 64) return launch_union_emit(tr, rt, o, s);
                     }
 #endif
+#ifdef EVICT_PRE_NW4   // measured 1.2% slower than 8-warp CTAs (ptxas keeps the static base in a register)
+                    if constexpr (EW == 2 && CL <= 4) {
+                        // 4-warp CTAs, static flag blocks (tree_union_cols' store addressing)
+                        auto pk = k_fused<NPL, IDF, KT, EW, CL, true, kWT, true, 4>;
+                        // (scratch blocks static: 4 × 8 KB; the dynamic part is records + ranks + stats)
+                        const size_t pdyn = fused_smem_bytes<G, kWT, 4>(rt->num_layers, rt->num_experts, flags, false) -
+                                            4 * fused_scratch_bytes<G>(rt->num_layers, rt->num_experts, flags);
+                        const int pt = (tr->batch + kWT - 1) / kWT;
+                        cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pdyn);
+                        pk<<<persistent_blocks(pk, pt, pdyn, 4 * 32), 4 * 32, pdyn, s>>>(*tr, cost, cs, pol, *rt, *o,
+                                                                                         ws, pt);
+                        return launched();
+                    }
+#endif
                     kern = k_fused<NPL, IDF, KT, EW, CL, true, kWT, true>;
                 } else {
                     kern = k_fused<NPL, IDF, KT, EW, CL, true>;
@@ -970,6 +1011,8 @@ struct FusedLauncher {
             }
         }
         const int ntiles = (tr->batch + wt - 1) / wt;
+        if (kern != k_fused<NPL, IDF, KT, EW, CL, false>)   // LEAN instantiations: no ranks area
+            dyn = fused_smem_bytes<G>(rt->num_layers, rt->num_experts, flags, false);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         const int blocks = persistent_blocks(kern, ntiles, dyn);
         kern<<<blocks, kWarps * 32, dyn, s>>>(*tr, cost, cs, pol, *rt, *o, ws, ntiles);

@@ -1388,10 +1388,10 @@ __device__ __forceinline__ uint32_t prmt_b32(uint32_t a, uint32_t b, uint32_t se
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
     return d;
 }
-__device__ __forceinline__ void ucols_store4(uint32_t fb, uint32_t w, uint32_t cb, uint32_t marker)
+__device__ __forceinline__ void ucols_store4(uint32_t fb, uint32_t w, uint32_t cb, uint32_t hb, uint32_t marker)
 {
     const uint32_t lo = (w & 0x03030303u) | cb;
-    const uint32_t hi = (w >> 2) & 0x1F1F1F1Fu;
+    const uint32_t hi = ((w >> 2) & 0x1F1F1F1Fu) | hb;   // hb < 128 per byte (row bits 5–6)
     // id j: byte 0 = lo.b_j, byte 1 = hi.b_j, bytes 2–3 = sign of hi.b_j (0)
     sts_u8(fb + prmt_b32(lo, hi, 0xCC40u), marker);
     sts_u8(fb + prmt_b32(lo, hi, 0xDD51u), marker);
@@ -1403,8 +1403,10 @@ __device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t 
                                                 int b, int N, int L, const void *__restrict__ ids,
                                                 uint8_t *flags, int32_t *__restrict__ union_count,
                                                 int32_t *__restrict__ union_total, int *epoch,
-                                                uint32_t *lsum, const UColsLane &ul)
+                                                uint32_t *lsum, const UColsLane &ul, uint32_t sbase, uint32_t hb)
 {
+    // byte stores at sbase + PRMT(lo, hi | hb): sbase = the flag block's shared address (hb = 0), or a
+    // CTA-uniform base with the block's 256-byte row offset in hb (the add folds into the STS)
     const int lane = lane_id();
     const int q = lane & 7, r0 = lane >> 3;
     const bool run = status == 0 && k > 0;
@@ -1429,8 +1431,7 @@ __device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t 
         for (int j0 = 0; j0 < k; j0 += UB) {
             uint2 x0[UB];
             uint32_t x1[UB], x2[UB];
-#pragma unroll
-            for (int u = 0; u < UB; u++) {
+            auto load = [&](int u) {
                 const uint32_t o = (uint32_t)klist[min(j0 + u, k - 1)] * rowB;
                 x0[u] = __ldg(reinterpret_cast<const uint2 *>(p0 + o));
                 x1[u] = 0u;
@@ -1442,20 +1443,30 @@ __device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t 
                     x1[u] = y.x;
                     x2[u] = y.y;
                 }
-            }
+            };
             // every row of the batch is consumed here, in the loads' own block: the compiler
             // cannot sink a row's loads behind the previous rows' stores (the store loop's
             // warp-uniform exits), so one DRAM round trip serves the batch (tail re-reads are
-            // rows k − 1 again: harmless for the id check)
+            // rows k − 1 again: harmless for the id check).  The batch's second half is loaded
+            // only when the tree has rows there (warp-uniform).
+            constexpr int H = UB > 4 ? UB / 2 : UB;
 #pragma unroll
-            for (int u = 0; u < UB; u++) badw |= x0[u].x | x0[u].y | x1[u] | x2[u];
+            for (int u = 0; u < H; u++) load(u);
+            if (UB > H && j0 + H < k) {
+#pragma unroll
+                for (int u = H; u < UB; u++) load(u);
+#pragma unroll
+                for (int u = H; u < UB; u++) badw |= x0[u].x | x0[u].y | x1[u] | x2[u];
+            }
+#pragma unroll
+            for (int u = 0; u < H; u++) badw |= x0[u].x | x0[u].y | x1[u] | x2[u];
 #pragma unroll
             for (int u = 0; u < UB; u++) {
                 if (j0 + u >= k) break;   // warp-uniform: a batch's tail re-read stores nothing
-                ucols_store4(fb, x0[u].x, cb0, marker);
-                ucols_store4(fb, x0[u].y, cb0, marker);
-                if constexpr (MODE >= 1) ucols_store4(fb, x1[u], cb1, marker);
-                if constexpr (MODE == 2) ucols_store4(fb, x2[u], cb1, marker);
+                ucols_store4(sbase, x0[u].x, cb0, hb, marker);
+                ucols_store4(sbase, x0[u].y, cb0, hb, marker);
+                if constexpr (MODE >= 1) ucols_store4(sbase, x1[u], cb1, hb, marker);
+                if constexpr (MODE == 2) ucols_store4(sbase, x2[u], cb1, hb, marker);
             }
         }
         __syncwarp();

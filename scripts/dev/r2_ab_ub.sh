@@ -1,0 +1,8 @@
+# A/B: union load batch 8 (default build) vs 4 (libevict_ub4.so), alternating, headline only
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x --tb=short -k "throughput or lean or stats" 2>&1 | grep -E "Error|assert|passed|failed" | head -5
+for i in 1 2; do
+for v in "" ub4; do
+EVICT_LIB_VARIANT=$v timeout 600 python bench.py --no-extras --steps 10 --warmup 3 --e2e-steps 1 --cpu-seconds 1 > gpurun_out/ab_$v$i.json 2>/dev/null
+python -c "import json;d=json.load(open('gpurun_out/ab_$v$i.json'));r=d['roofline'];print('AB', '$v', r['kernel_ms'], r['frac'])"
+done; done
