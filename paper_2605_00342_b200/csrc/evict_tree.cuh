@@ -1398,13 +1398,52 @@ __device__ __forceinline__ void ucols_store4(uint32_t fb, uint32_t w, uint32_t c
     sts_u8(fb + prmt_b32(lo, hi, 0xEE62u), marker);
     sts_u8(fb + prmt_b32(lo, hi, 0xFF73u), marker);
 }
+// One load batch of UB kept rows (this lane's parts) and the loader: rows j0 .. j0 + UB − 1 of
+// the tree (a slot past k re-reads row k − 1); `half` loads only the first UB / 2 when the rest
+// lies past k (warp-uniform).
+template <int UB>
+struct UColsBatch {
+    uint2 x0[UB];
+    uint32_t x1[UB], x2[UB];
+};
+template <int MODE, int UB>
+__device__ __forceinline__ void ucols_load(UColsBatch<UB> &v, const uint8_t *__restrict__ klist, int k, int j0,
+                                           int b, int N, int L, const void *__restrict__ ids, int lane)
+{
+    const uint32_t rowB = (uint32_t)L * 8u;
+    const bool ld0 = lane < L;
+    const bool ld1 = MODE == 1 ? lane < 2 * (L - 32) : (MODE == 2 ? lane < L - 32 : false);
+    const uint32_t lo0 = ld0 ? 8u * (uint32_t)lane : 0u;
+    const uint32_t lo1 = ld1 ? (MODE == 1 ? 256u + 4u * (uint32_t)lane : 256u + 8u * (uint32_t)lane) : 0u;
+    const uint8_t *tb = reinterpret_cast<const uint8_t *>(ids) + (size_t)b * N * rowB;
+    const uint8_t *p0 = tb + lo0, *p1 = tb + lo1;
+#pragma unroll
+    for (int u = 0; u < UB; u++) {
+        const uint32_t o = (uint32_t)klist[min(j0 + u, k - 1)] * rowB;
+        v.x0[u] = __ldg(reinterpret_cast<const uint2 *>(p0 + o));
+        v.x1[u] = 0u;
+        v.x2[u] = 0u;
+        if constexpr (MODE == 1) {
+            v.x1[u] = __ldg(reinterpret_cast<const uint32_t *>(p1 + o));
+        } else if constexpr (MODE == 2) {
+            const uint2 y = __ldg(reinterpret_cast<const uint2 *>(p1 + o));
+            v.x1[u] = y.x;
+            v.x2[u] = y.y;
+        }
+    }
+}
 template <int MODE, int UB>
 __device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t *__restrict__ klist, int k,
                                                 int b, int N, int L, const void *__restrict__ ids,
                                                 uint8_t *flags, int32_t *__restrict__ union_count,
                                                 int32_t *__restrict__ union_total, int *epoch,
-                                                uint32_t *lsum, const UColsLane &ul, uint32_t sbase, uint32_t hb)
+                                                uint32_t *lsum, const UColsLane &ul, uint32_t sbase, uint32_t hb,
+                                                UColsBatch<UB> *pf = nullptr, const uint8_t *nklist = nullptr,
+                                                int nk = 0, int nb = 0)
 {
+    // pf (cross-tree prefetch): on entry it holds this tree's first batch (loaded during the
+    // previous tree's read-back); after this tree's stores it receives the next tree's first batch
+    // (nklist / nk / nb; nk = 0: none) so that round trip overlaps this read-back.
     // byte stores at sbase + PRMT(lo, hi | hb): sbase = the flag block's shared address (hb = 0), or a
     // CTA-uniform base with the block's 256-byte row offset in hb (the add folds into the STS)
     const int lane = lane_id();
@@ -1429,6 +1468,20 @@ __device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t 
         uint32_t badw = 0u;
 #pragma unroll 1
         for (int j0 = 0; j0 < k; j0 += UB) {
+            if (pf != nullptr && j0 == 0) {
+                // the batch arrived during the previous tree; its id check
+#pragma unroll
+                for (int u = 0; u < UB; u++) badw |= pf->x0[u].x | pf->x0[u].y | pf->x1[u] | pf->x2[u];
+#pragma unroll
+                for (int u = 0; u < UB; u++) {
+                    if (u >= k) break;   // warp-uniform
+                    ucols_store4(sbase, pf->x0[u].x, cb0, hb, marker);
+                    ucols_store4(sbase, pf->x0[u].y, cb0, hb, marker);
+                    if constexpr (MODE >= 1) ucols_store4(sbase, pf->x1[u], cb1, hb, marker);
+                    if constexpr (MODE == 2) ucols_store4(sbase, pf->x2[u], cb1, hb, marker);
+                }
+                continue;
+            }
             uint2 x0[UB];
             uint32_t x1[UB], x2[UB];
             auto load = [&](int u) {
@@ -1469,6 +1522,7 @@ __device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t 
                 if constexpr (MODE == 2) ucols_store4(sbase, x2[u], cb1, hb, marker);
             }
         }
+        if (pf != nullptr && nk > 0) ucols_load<MODE, UB>(*pf, nklist, nk, 0, nb, N, L, ids, lane);
         __syncwarp();
         const bool clear = ep == 1;
         uint32_t a0 = 0u, a1 = 0u, a2 = 0u, a3 = 0u, c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u;
@@ -1513,6 +1567,7 @@ __device__ __forceinline__ void tree_union_cols(uint32_t &status, const uint8_t 
             cnt[0] = cnt[1] = cnt[2] = cnt[3] = 0u;
         }
     }
+    if (!run && pf != nullptr && nk > 0) ucols_load<MODE, UB>(*pf, nklist, nk, 0, nb, N, L, ids, lane);
     // union counts (zeros for an errored tree)
     if (ul.nl < 4) cnt[3] = 0u;
     if (ul.nl < 3) cnt[2] = 0u;
