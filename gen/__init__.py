@@ -115,6 +115,17 @@ def _p(a):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
+GEN_MAX_TOPK, GEN_MAX_POOL = 16, 1024   # evict_gen.h
+
+
+def check_tree_shape(steps, topk):
+    """The generator's candidate pool (topk + (steps − 1)·topk² candidates) lives in fixed scratch
+    arrays (evict_gen.h GEN_MAX_POOL): reject shapes that would overflow them."""
+    if not (1 <= topk <= GEN_MAX_TOPK) or steps < 1 or topk + (steps - 1) * topk * topk > GEN_MAX_POOL:
+        raise ValueError(f"draft-tree shape steps={steps} topk={topk} exceeds the generator's pool "
+                         f"({GEN_MAX_POOL} candidates, topk <= {GEN_MAX_TOPK})")
+
+
 def _fan(fn, B, threads):
     threads = max(1, min(threads, B))
     step = (B + threads - 1) // threads
@@ -129,6 +140,7 @@ def _fan(fn, B, threads):
 # ---------------------------------------------------------------- host side
 def trees(seed, B, N, steps, topk, tree_base=0, m_lo=M_LO, m_hi=M_HI, threads=8):
     """EAGLE-style draft trees: (parent int32 [B][N], q float32 [B][N], n_nodes int32 [B])."""
+    check_tree_shape(steps, topk)
     parent = np.empty((B, N), np.int32)
     q = np.empty((B, N), np.float32)
     n = np.empty(B, np.int32)
@@ -205,6 +217,7 @@ def _stream():
 
 def trees_cuda(seed, B, N, steps, topk, tree_base=0, m_lo=M_LO, m_hi=M_HI, device="cuda"):
     import torch
+    check_tree_shape(steps, topk)
     L = cuda_lib()
     parent = torch.empty((B, N), dtype=torch.int32, device=device)
     q = torch.empty((B, N), dtype=torch.float32, device=device)

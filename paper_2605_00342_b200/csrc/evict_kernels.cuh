@@ -941,6 +941,7 @@ __global__ void __launch_bounds__(WPC * 32) k_fused_lat(evict_trees_t tr, const 
     uint32_t st = t.status;
     int epoch = 0;
     __syncwarp();
+    // (tree_union_cols measured 8% slower here at batch 64: 11.2 vs 10.3 µs per graph replay)
     if constexpr (EW == 2)
         tree_union_flags64<1, CL, true, false, false, 8>(st, sm.klist, k, b, N, L, E, rt.ids, flags,
                                                          out.union_count, out.union_total, nullptr, &epoch);
@@ -1002,12 +1003,6 @@ struct FusedLauncher {
                     k_scan_offsets<<<(tr->batch + kScanChunk - 1) / kScanChunk, 1024, 0, s>>>(
                         tr->batch, o->k_star, chunk_sums, o->verify_offsets);
                     if (cudaGetLastError() != cudaSuccess) return EVICT_ERR_CUDA;
-#ifdef EVICT_UE
-                    if constexpr (NPL == 2 && EW == 2) {
-                        // A6 + A7 (+ A9): warp per tree, lane-owned flag columns (union_emit.cu)
-                        if (rt->num_layers <= 64) return launch_union_emit(tr, rt, o, s);
-                    }
-#endif
 #ifdef EVICT_PRE_NW4   // measured 1.2% slower than 8-warp CTAs (ptxas keeps the static base in a register)
                     if constexpr (EW == 2 && CL <= 4) {
                         // 4-warp CTAs, static flag blocks (tree_union_cols' store addressing)

@@ -26,9 +26,6 @@ constexpr int kFusedTileTrees = 4;   // trees per warp tile of k_fused
 constexpr int kFusedSmallBatch = 2048;   // k_fused LEAN takes one-tree tiles up to this batch
 int dev_sms();
 bool dev_supported();   // the current device is sm_100 (B200); else every entry point returns UNSUPPORTED
-// throughput path's A6 + A7 (+ A9) after k_select_g / k_scan_offsets (u8 top-8, E = 128, L ≤ 64, N ≤ 64)
-evict_status_t launch_union_emit(const evict_trees_t *, const evict_routing_t *, const evict_fused_out_t *,
-                                 cudaStream_t);
 template <int NPL> evict_status_t launch_select(EVICT_SELECT_ARGS);
 template <int NPL> evict_status_t launch_build(EVICT_BUILD_ARGS);
 template <int NPL> evict_status_t launch_union(EVICT_UNION_ARGS);

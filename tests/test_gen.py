@@ -82,3 +82,18 @@ def test_device_generator_matches_host():
     w = gen.wgate(3, 2, 128, 128, mode=1, scale_log2=-5)
     tw = gen.wgate_cuda(3, 2, 128, 128, mode=1, scale_log2=-5)
     assert (tw.view(torch.int16).cpu().numpy().view(np.uint16) == w).all()
+
+
+def test_tree_shape_guard():
+    """Draft-tree shapes whose candidate pool (topk + (steps − 1)·topk²) exceeds the generator's
+    fixed scratch are rejected before any C code runs (8 steps × topk 16 = 1808 > 1024 once
+    corrupted the host heap); the benchmark shapes fit."""
+    import pytest
+    with pytest.raises(ValueError):
+        gen.trees(4, 2, 128, 8, 16)
+    with pytest.raises(ValueError):
+        gen.trees(4, 2, 60, 2, 17)
+    for steps, topk in ((6, 10), (8, 10), (1, 16)):
+        gen.check_tree_shape(steps, topk)
+    P, Q, n = gen.trees(4, 2, 128, 8, 10)
+    assert P.shape == (2, 128) and (n >= 1).all()
