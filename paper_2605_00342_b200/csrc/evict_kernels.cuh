@@ -427,17 +427,22 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : 3) k_fused(evict_trees_
     // NW == 4: the 4 scratch (= flag) blocks are static shared memory, so their address is a link-time
     // constant the compiler folds into every byte store's immediate; the dynamic block holds the rest
     uint8_t *scr_base = dsm;
-    size_t dyn_scr = (size_t)NW * scratch;
+    uint32_t sfold_static = 0u;
+    EmitRec<G> *rec_base = reinterpret_cast<EmitRec<G> *>(dsm + (size_t)NW * scratch);
+    uint8_t *ranks = reinterpret_cast<uint8_t *>(dsm + (size_t)NW * scratch) + align16(sizeof(EmitRec<G>) * NW * WT);
+    FusedStats *fs = reinterpret_cast<FusedStats *>(ranks + (LEAN ? 0 : align16((size_t)NW * TPW * NMAX)));
     if constexpr (NW == 4) {
+        // the 4 × 8 KB flag blocks are the kernel's only static shared memory (offset 0 of the
+        // CTA's window: the base add vanishes from every byte store); records + stats dynamic
         __shared__ __align__(16) uint8_t s_scr4[4 * 8192];
         scr_base = s_scr4;
-        dyn_scr = 0;
+        sfold_static = (uint32_t)__cvta_generic_to_shared(s_scr4);   // the symbol itself: a constant
+        rec_base = reinterpret_cast<EmitRec<G> *>(dsm);
+        fs = reinterpret_cast<FusedStats *>(dsm + align16(sizeof(EmitRec<G>) * NW * WT));
     }
     uint8_t *wscr = scr_base + (size_t)warp * scratch;
-    EmitRec<G> *rec = reinterpret_cast<EmitRec<G> *>(dsm + dyn_scr) + warp * WT;
-    uint8_t *ranks = reinterpret_cast<uint8_t *>(dsm + dyn_scr) + align16(sizeof(EmitRec<G>) * NW * WT);
+    EmitRec<G> *rec = rec_base + warp * WT;
     uint8_t *rk = ranks + ((size_t)warp * TPW + gi) * NMAX;
-    FusedStats *fs = reinterpret_cast<FusedStats *>(ranks + (LEAN ? 0 : align16((size_t)NW * TPW * NMAX)));
     // A9 folded into the launch: the single-pass E = 128 LEAN union (the caller passes out.stats
     // only for that configuration; it runs evict_batch_stats after the launch otherwise)
     constexpr bool kFold = LEAN && EW == 2 && CL <= 4;
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : 3) k_fused(evict_trees_
     // block): byte stores at the CTA-uniform base sfold + a PRMT result whose row byte carries 32·warp
     // (hfold); otherwise at this warp's block (sfold = its address, hfold = 0)
     constexpr bool fold = NW == 4;
-    const uint32_t sfold = (uint32_t)__cvta_generic_to_shared(fold ? scr_base : wscr);
+    const uint32_t sfold = fold ? sfold_static : (uint32_t)__cvta_generic_to_shared(wscr);
     const uint32_t hfold = fold ? (32u * (uint32_t)warp) * 0x01010101u : 0u;
     if constexpr (kFold) {
         if (fstats) {
@@ -1007,9 +1012,7 @@ struct FusedLauncher {
                     if constexpr (EW == 2 && CL <= 4) {
                         // 4-warp CTAs, static flag blocks (tree_union_cols' store addressing)
                         auto pk = k_fused<NPL, IDF, KT, EW, CL, true, kWT, true, 4>;
-                        // (scratch blocks static: 4 × 8 KB; the dynamic part is records + ranks + stats)
-                        const size_t pdyn = fused_smem_bytes<G, kWT, 4>(rt->num_layers, rt->num_experts, flags, false) -
-                                            4 * fused_scratch_bytes<G>(rt->num_layers, rt->num_experts, flags);
+                        const size_t pdyn = align16(sizeof(EmitRec<G>) * 4 * kWT) + kStatsSmem;   // flags static
                         const int pt = (tr->batch + kWT - 1) / kWT;
                         cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pdyn);
                         pk<<<persistent_blocks(pk, pt, pdyn, 4 * 32), 4 * 32, pdyn, s>>>(*tr, cost, cs, pol, *rt, *o,
