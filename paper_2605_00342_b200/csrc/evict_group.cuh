@@ -607,12 +607,20 @@ __device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W]
         if (slot_of != nullptr) {
             const int g = gl<G>();
             const int kk = emit ? k : 0;
-            for (int s = g; s < kk; s += G) child[s] = 0ull;
-            __syncwarp();
-            for (int s = g; s < kk; s += G) {
-                const int i = klist[s];
-                if (i > 0)
-                    atomicOr(reinterpret_cast<unsigned long long *>(&child[slot_of[par[i]]]), 1ull << s);
+            // small kept sets (the cost-effective cut: k* ≈ 8): first child and next sibling by a
+            // scan of the later slots (children and later siblings have larger node indices, so
+            // larger slots) — no shared atomics; large kept sets build child masks instead
+            constexpr int kScanMax = 16;
+            const bool scan = kk <= kScanMax;
+            if (!scan)
+                for (int s = g; s < kk; s += G) child[s] = 0ull;
+            __syncwarp();   // (outside the group-dependent branches: every lane of the warp arrives)
+            if (!scan) {
+                for (int s = g; s < kk; s += G) {
+                    const int i = klist[s];
+                    if (i > 0)
+                        atomicOr(reinterpret_cast<unsigned long long *>(&child[slot_of[par[i]]]), 1ull << s);
+                }
             }
             __syncwarp();
             for (int s = g; s < kk; s += G) {
@@ -623,12 +631,21 @@ __device__ __forceinline__ void g_emit(const uint64_t (&keep)[grp::GShape<G>::W]
                     depth++;
                     row |= 1ull << slot_of[a];
                 }
-                const uint64_t cm = child[s];
-                const int nt = cm ? __ffsll((long long)cm) - 1 : -1;
-                int ns = -1;
-                if (i > 0) {
-                    const uint64_t sib = child[slot_of[par[i]]] & (s >= 63 ? 0ull : (~0ull << (s + 1)));
-                    ns = sib ? __ffsll((long long)sib) - 1 : -1;
+                int nt = -1, ns = -1;
+                if (scan) {
+                    const int p = i > 0 ? par[i] : -2;
+                    for (int t = s + 1; t < kk; t++) {
+                        const int pj = par[klist[t]];
+                        if (nt < 0 && pj == i) nt = t;
+                        if (ns < 0 && pj == p) ns = t;
+                    }
+                } else {
+                    const uint64_t cm = child[s];
+                    nt = cm ? __ffsll((long long)cm) - 1 : -1;
+                    if (i > 0) {
+                        const uint64_t sib = child[slot_of[par[i]]] & (s >= 63 ? 0ull : (~0ull << (s + 1)));
+                        ns = sib ? __ffsll((long long)sib) - 1 : -1;
+                    }
                 }
                 const int rowi = off + s;
                 if (kept_index) kept_index[rowi] = i;
