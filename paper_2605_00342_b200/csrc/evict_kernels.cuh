@@ -448,6 +448,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : 3) k_fused(evict_trees_
     constexpr bool kFold = LEAN && EW == 2 && CL <= 4;
     const bool fstats = kFold && out.stats != nullptr;
     uint32_t lsum[4] = {0u, 0u, 0u, 0u};   // folded A9: this lane's output layers ulane.l0 + m
+    unsigned rs_tr = 0u, rs_k = 0u, rs_n = 0u, rs_err = 0u;   // folded A9 scalars (lane 0, registers)
+    double rs_e = 0.0, rs_u = 0.0;
+    bool emit_dirty = false;   // PRE: the last tile's emit wrote child masks into the flag prefix
     const UColsLane ulane = ucols_lane<CL == 4 ? 2 : 1>(lane, rt.num_layers);
     // NW == 4 (the PRE launch: union_count given, E = 128, so every scratch block is the 8 KB flag
     // block): byte stores at the CTA-uniform base sfold + a PRMT result whose row byte carries 32·warp
@@ -578,7 +581,8 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : 3) k_fused(evict_trees_
                 uint4 *f4 = reinterpret_cast<uint4 *>(wscr);
                 const int nflag = union_flag_bytes(L, E) / 16;   // uint4 words
                 constexpr int dirty = (int)(fused_scratch_dirty<G>() / 16);
-                const int nz = first ? nflag : (dirty < nflag ? dirty : nflag);
+                // (PRE: only the emit writes the prefix, and only for kept sets > 16 — its child masks)
+                const int nz = first ? nflag : ((PRE && !emit_dirty) ? 0 : (dirty < nflag ? dirty : nflag));
                 for (int i = lane; i < nz; i += 32) f4[i] = make_uint4(0u, 0u, 0u, 0u);
                 __syncwarp();
                 first = false;
@@ -614,16 +618,15 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : 3) k_fused(evict_trees_
                                                                    pfp, rec[nx ? slot + 1 : slot].klist, nk, b + 1);
                     if constexpr (kFold) {
                         if (fstats && lane == 0) {
-                            unsigned *wsc = fs->sc[warp];
-                            wsc[0] += 1u;
+                            rs_tr += 1u;
                             if (st) {
-                                wsc[3] += 1u;
+                                rs_err += 1u;
                                 atomicAdd(&fs->hist[0], 1u);
                             } else {
-                                wsc[1] += (unsigned)er.k;
-                                wsc[2] += (unsigned)er.n;
-                                fs->d[warp][0] += (double)er.ehat;
-                                fs->d[warp][1] += (double)er.util;
+                                rs_k += (unsigned)er.k;
+                                rs_n += (unsigned)er.n;
+                                rs_e += (double)er.ehat;
+                                rs_u += (double)er.util;
                                 atomicAdd(&fs->hist[er.k], 1u);
                             }
                         }
@@ -675,6 +678,9 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : 3) k_fused(evict_trees_
                            (active && out.pos_offset) ? __ldg(out.pos_offset + b) : 0, er.par,
                            child, er.klist, out.kept_index, out.retrieve_index, out.positions,
                            out.next_token, out.next_sibling, out.tree_mask, W == 1 ? er.slot : nullptr);
+            // (g_emit writes child masks into the prefix unless W = 1 and k ≤ 16)
+            if (pass == 0) emit_dirty = false;
+            emit_dirty |= __any_sync(kFull, W != 1 || (active && k > 16));
             __syncwarp();
         }
         EVICT_PHASE(4);
@@ -682,6 +688,10 @@ __global__ void __launch_bounds__(NW * 32, NW == 4 ? 6 : 3) k_fused(evict_trees_
     }
     if constexpr (kFold) {
         if (fstats) {
+            if (lane == 0) {
+                fs->sc[warp][0] = rs_tr; fs->sc[warp][1] = rs_k; fs->sc[warp][2] = rs_n; fs->sc[warp][3] = rs_err;
+                fs->d[warp][0] = rs_e; fs->d[warp][1] = rs_u;
+            }
             // per-lane layer sums (tree_union_cols' output layers)
 #pragma unroll
             for (int m = 0; m < 4; m++)
