@@ -499,11 +499,12 @@ def test_fused_reads_pinned_host_routing(ev, B):
                                       (40, None), (48, ("fixed", 50)), (48, ("coverage", 0.9)),
                                       (56, None), (64, ("fixed", 45))])
 def test_throughput_union_emit_modes(ev, L, policy):
-    """The throughput path's union/emit kernel (k_union_emit, B > 2048, u8 top-8, E = 128, N ≤ 64)
-    in its three flag-region layouts (L ≤ 32; 32 < L ≤ 48 half-layer columns; L ≤ 64 layer
-    columns), ragged trees, kept sets reaching nodes ≥ 32 (fixed k / coverage policies: the emit's
-    second node half), an errored tree (NaN q) and a BAD_EXPERT row; A9 statistics folded into
-    the launch must equal the oracle's batch_stats over the call's own outputs."""
+    """The throughput path's union/emit kernel (k_fused PRE with tree_union_cols; B > 2048, u8
+    top-8, E = 128, N ≤ 64) over its flag-column layouts (L ≤ 48: region 1 in half-layer columns,
+    empty for L ≤ 32; L ≤ 64: layer columns), ragged trees, kept sets reaching nodes ≥ 32 and
+    k > 16 (fixed k / coverage policies: the emit's child-mask path), an errored tree (NaN q) and a
+    BAD_EXPERT row; A9 statistics folded into the launch must equal the oracle's batch_stats over
+    the call's own outputs."""
     c = gen.CONFIGS["c2"]
     B, N, E, K = 4500, c["N"], 128, 8
     P, Q, n = gen.trees(c["seed"] + L, B, N, c["steps"], c["topk"])
